@@ -1,0 +1,91 @@
+"""Drop-in replacement for `meshpipe._core` (reference _core/__init__.py:1-20).
+
+`dp_sweep` keeps the exact 15-argument signature and return tuple of the
+reference operator (_dp.pyx:14-28; dp_py.py:27-43): numpy inputs in the
+DpTables layout, numpy outputs F, N (float64) and bp_i, bp_o (int32) of shape
+[s_max+1, L+2, G+1].  The sweep runs on the GPU (hapt_tables_finalize +
+hapt_dp_sweep_batch with full outputs); a reference caller such as
+planner.dp_search or benchmarks/bench_dp.py can be pointed at it unchanged:
+
+    import meshpipe.planner as P, paper_2509_24859_b200._core as C
+    P.dp_sweep = C.dp_sweep
+
+There is no CPU fallback: without the CUDA library this module raises.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .engine import DeviceTables, Sweeper
+
+BACKEND = "cuda"
+
+_cache: dict = {}
+
+
+def _check_encoding(g_mesh: np.ndarray, g_avail: np.ndarray, opt_off: np.ndarray) -> None:
+    """The device kernel reads the successor state's boundary row from g alone,
+    which holds for the DpTables encoding (planner.py:213-226): meshes consumed
+    in order, g_avail counting up inside each mesh."""
+    G = len(g_mesh) - 1
+    for g in range(1, G + 1):
+        m = int(g_mesh[g])
+        if g > 1 and int(g_mesh[g - 1]) != m:
+            if int(g_mesh[g - 1]) != m + 1 or int(g_avail[g]) != 1:
+                raise ValueError("dp_sweep: unsupported remaining-device encoding")
+        elif g > 1 and int(g_avail[g]) != int(g_avail[g - 1]) + 1:
+            raise ValueError("dp_sweep: unsupported remaining-device encoding")
+        if not 0 <= m < len(opt_off) - 1:
+            raise ValueError("dp_sweep: g_mesh out of range")
+    if G >= 1 and int(g_avail[1]) != 1:
+        raise ValueError("dp_sweep: unsupported remaining-device encoding")
+
+
+def _device_tables(args: dict, s_max: int) -> DeviceTables:
+    """Tables are cached on the identity of the caller's arrays (DpTables keeps
+    them alive for a whole search), so repeated sweeps skip the upload."""
+    key = tuple(id(args[k]) for k in sorted(args)) + (s_max,)
+    hit = _cache.get(key)
+    if hit is not None and all(hit[1][k] is args[k] for k in args):
+        return hit[0]
+    L = args["t_tab"].shape[1] - 2
+    G = args["g_mesh"].shape[0] - 1
+    n_opts = args["t_tab"].shape[0]
+    n_meshes = args["cb_same"].shape[0]
+    dt = DeviceTables(L, G, n_opts, n_meshes).load_dense(args, s_max)
+    _cache.clear()
+    _cache[key] = (dt, dict(args), Sweeper(dt))
+    return dt
+
+
+def dp_sweep(t_max, t_tab, mp_tab, ma_tab, opt_cap, opt_mesh, opt_devs, opt_off, cb_same,
+             cb_next, g_mesh, g_avail, s_max, span_off, span_items):
+    """One t_max candidate through the stage-partition DP (_dp.pyx:48-95)."""
+    t_tab = np.asarray(t_tab)
+    for name, arr, dt, nd in (
+        ("t_tab", t_tab, np.float64, 3), ("mp_tab", mp_tab, np.float64, 3),
+        ("ma_tab", ma_tab, np.float64, 3), ("opt_cap", opt_cap, np.float64, 1),
+        ("opt_mesh", opt_mesh, np.int32, 1), ("opt_devs", opt_devs, np.int32, 1),
+        ("opt_off", opt_off, np.int32, 1), ("cb_same", cb_same, np.float64, 2),
+        ("cb_next", cb_next, np.float64, 2), ("g_mesh", g_mesh, np.int32, 1),
+        ("g_avail", g_avail, np.int32, 1), ("span_off", span_off, np.int32, 1),
+        ("span_items", span_items, np.int32, 1),
+    ):
+        a = np.asarray(arr)
+        if a.dtype != dt or a.ndim != nd:
+            # the Cython memoryviews reject these the same way
+            raise ValueError(f"Buffer dtype mismatch for {name}: expected {np.dtype(dt)} "
+                             f"with {nd} dims, got {a.dtype} with {a.ndim}")
+    s_max = int(s_max)
+    args = dict(t_tab=t_tab, mp_tab=mp_tab, ma_tab=ma_tab, opt_cap=opt_cap, opt_mesh=opt_mesh,
+                opt_devs=opt_devs, opt_off=opt_off, cb_same=cb_same, cb_next=cb_next,
+                g_mesh=g_mesh, g_avail=g_avail, span_off=span_off, span_items=span_items)
+    _check_encoding(np.asarray(g_mesh), np.asarray(g_avail), np.asarray(opt_off))
+    dt = _device_tables(args, s_max)
+    sw = next(iter(_cache.values()))[2]
+    F, N, bpi, bpo = sw.full_tables(float(t_max))
+    return F.cpu().numpy(), N.cpu().numpy(), bpi.cpu().numpy(), bpo.cpu().numpy()
+
+
+__all__ = ["dp_sweep", "BACKEND"]

@@ -1,0 +1,76 @@
+// Shared helpers for the HAPT B200 kernels (sm_100a).
+//
+// Every floating-point expression that the reference evaluates in Python /
+// Cython is written with explicit round-to-nearest intrinsics (__dadd_rn,
+// __dmul_rn, __ddiv_rn) so that nvcc can never contract it into an FMA; the
+// library is additionally compiled with --fmad=false.  This is what makes the
+// device tables and DP values bit-identical to the CPU reference
+// (SURVEY.md Appendix A).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/hapt_b200.h"
+
+namespace hapt {
+
+constexpr double kInf = __builtin_huge_val();
+constexpr int kKSat = 65535;  // saturation of the integer memory threshold
+
+void set_error(const char *fmt, ...);
+void *tables_hist(const hapt_tables *t);  // rank-histogram scratch of a tables buffer
+
+inline int cuda_status(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return HAPT_OK;
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return HAPT_ECUDA;
+}
+
+#define HAPT_CUDA(call)                                           \
+  do {                                                            \
+    int _st = ::hapt::cuda_status((call), #call);                 \
+    if (_st != HAPT_OK) return _st;                               \
+  } while (0)
+
+#define HAPT_LAUNCHED(what)                                       \
+  do {                                                            \
+    int _st = ::hapt::cuda_status(cudaGetLastError(), what);      \
+    if (_st != HAPT_OK) return _st;                               \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+inline unsigned grid_for(size_t n, unsigned block) {
+  size_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+// Exact memory mask of _dp.pyx:83 turned into an integer threshold: the
+// largest integer K in [0, kKSat] with  !(mp + K*ma > cap)  for every
+// integer in [1, K].  fl(mp + fl(K*ma)) is monotone non-decreasing in K for
+// ma >= 0 (round-to-nearest is monotone), so the admissible K form a prefix
+// and  kk <= kmax  is bit-equivalent to the reference test.
+__device__ __forceinline__ bool mem_ok(double mp, double ma, double cap, int K) {
+  return !(__dadd_rn(mp, __dmul_rn((double)K, ma)) > cap);
+}
+
+__device__ __forceinline__ int mem_kmax(double mp, double ma, double cap) {
+  if (!mem_ok(mp, ma, cap, 1)) return 0;
+  if (mem_ok(mp, ma, cap, kKSat)) return kKSat;
+  int lo = 1, hi = kKSat;  // ok(lo), !ok(hi)
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (mem_ok(mp, ma, cap, mid)) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Positive IEEE doubles order like their bit patterns.
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  return (unsigned long long)__double_as_longlong(x);
+}
+
+}  // namespace hapt

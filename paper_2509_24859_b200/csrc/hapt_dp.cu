@@ -1,0 +1,523 @@
+// K2 -- the stage-partition DP, batched over t_max candidates.
+//
+// Reference operator: meshpipe._core.dp_sweep (_dp.pyx:48-95), called once per
+// candidate by planner.dp_search (planner.py:397-413).
+//
+//   F[s,k,g] = min over options o of mesh g_mesh[g] with opt_devs[o] <= g_avail[g],
+//              and feasible spans i in CSR(o,k) (ascending), of
+//              tt + (2c + F[s-1,i+1,g-devs])   subject to  tt <= t_max, c <= t_max,
+//              F[s-1,..] finite, mp + kk*ma <= cap,  kk = ceil(2c/t_max)+1+N[s-1,i+1,g2]
+//   ties: first strictly smaller in (o asc, i asc) order.
+//
+// B200 mapping:
+//  * layer-synchronous sweep: F[s] reads only F[s-1], so one launch per layer
+//    processes every (k,g) cell of every candidate in the batch;
+//  * a warp = one cell for 32 candidates: lanes are candidates, so the loop
+//    over (o, i) is warp-uniform, the CSR entry loads are broadcasts, and each
+//    lane runs exactly the reference's scan order with strict '<' -- tie
+//    semantics are preserved by construction, no cross-lane argmin needed;
+//  * the previous layer is kept as a per-(state, split) "successor" table
+//    H = 2c + F[s-1] (+inf when F is infinite or c > t_max) and
+//    KK = ceil(2c/t_max) + 1 + N[s-1], candidate-innermost so that a warp's
+//    32 lanes read 256 contiguous bytes; it is written by the epilogue of the
+//    previous layer's launch (fused; no separate pass);
+//  * the masks tt <= t_max and mp + kk*ma <= cap become integer compares
+//    (pool rank, exact integer memory threshold); a row suffix-min of the
+//    rank lets a warp stop a row once no lane can accept a later span;
+//  * provably infinite cells/transitions (g < s, L-k+1 < s, i > L-s+1,
+//    g2 < s-1) are never visited.
+#include "hapt_common.cuh"
+
+namespace hapt {
+namespace {
+
+constexpr int kWarps = 8;  // warps (cells) per block
+
+struct Batch {
+  // tables
+  const hapt_span *spans;
+  const hapt_span_ik *span_ik;
+  const int32_t *span_off, *opt_off, *opt_devs, *g_mesh, *g_avail, *g_crow;
+  const double *cb;    // cb_same rows then cb_next rows, [2*n_meshes][L+1]
+  const double *pool;
+  const int64_t *counters;
+  int L, G, s_max, n_cand, n_groups;
+  size_t hg;           // (G+1)*(L+1) successor entries per candidate group
+  // per batch
+  const double *tmax;  // [n_cand]
+  double *tmax_pad;    // [n_groups*32]
+  int32_t *tcnt;       // [n_groups*32]  #pool values <= t_max
+  int32_t *gmax;       // [n_groups]     max tcnt in the group
+  double *H[2];
+  uint16_t *K[2];
+  double *ftop;
+  unsigned long long *states;
+  hapt_dp_full full;
+};
+
+struct WsLayout {
+  size_t tmax_pad, tcnt, gmax, H0, H1, K0, K1, total;
+};
+
+WsLayout ws_layout(const hapt_tables *t, int n_cand) {
+  WsLayout w{};
+  const size_t ng = (size_t)(n_cand + 31) / 32, np = ng * 32;
+  const size_t hg = (size_t)(t->G + 1) * (t->L + 1);
+  size_t cur = 0;
+  w.tmax_pad = cur; cur += align_up(np * 8);
+  w.tcnt = cur; cur += align_up(np * 4);
+  w.gmax = cur; cur += align_up(ng * 4);
+  w.H0 = cur; cur += align_up(ng * hg * 32 * 8);
+  w.H1 = cur; cur += align_up(ng * hg * 32 * 8);
+  w.K0 = cur; cur += align_up(ng * hg * 32 * 2);
+  w.K1 = cur; cur += align_up(ng * hg * 32 * 2);
+  w.total = cur;
+  return w;
+}
+
+__device__ __forceinline__ int upper_bound(const double *a, int n, double v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Candidate padding, pool ranks, and the layer-0 successor table:
+// F[0, L+1, 0] = 0 (_dp.pyx:41) is the only finite base state.
+__global__ void dp_prep(Batch b) {
+  const int lane = threadIdx.x & 31;
+  const int group = blockIdx.x;
+  const int cand = group * 32 + lane;
+  const int src = cand < b.n_cand ? cand : b.n_cand - 1;
+  const double tm = b.tmax[src];
+  const int plen = (int)b.counters[1];
+  const int cnt = upper_bound(b.pool, plen, tm);
+  if (threadIdx.x < 32) {
+    b.tmax_pad[cand] = tm;
+    b.tcnt[cand] = cnt;
+    int m = cnt;
+    for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (lane == 0) b.gmax[group] = m;
+  }
+  // layer-0 table for this group: everything +inf except (g2 = 0, i = L)
+  double *H = b.H[0] + (size_t)group * b.hg * 32;
+  uint16_t *K = b.K[0] + (size_t)group * b.hg * 32;
+  for (size_t x = threadIdx.x; x < b.hg * 32; x += blockDim.x) {
+    H[x] = kInf;
+    K[x] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int row = b.g_crow[0];
+    const double c = b.cb[(size_t)row * (b.L + 1) + b.L];
+    const size_t e = (size_t)b.L * 32 + lane;  // g2 = 0, i = L
+    if (c <= tm) {
+      const double c2 = __dmul_rn(2.0, c);
+      H[e] = __dadd_rn(c2, 0.0);
+      K[e] = (uint16_t)((int)ceil(__ddiv_rn(c2, tm)) + 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) dp_relax(Batch b, int s, int group0) {
+  __shared__ int fin_cnt[kWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int group = group0 + blockIdx.y;
+  const int L = b.L, G = b.G;
+  const int nk = L - s + 1, ng = G - s + 1;
+  const long cell = (long)blockIdx.x * kWarps + warp;
+  const bool active = cell < (long)nk * ng;
+  const int cand = group * 32 + lane;
+  int fin = 0;
+  if (active) {
+    const int k = 1 + (int)(cell % nk);
+    const int g = s + (int)(cell / nk);
+    const double tm = b.tmax_pad[cand];
+    const int cnt = b.tcnt[cand];
+    const int maxcnt = b.gmax[group];
+    const int imax = L - s + 1;
+    const int r = b.g_mesh[g], avail = b.g_avail[g];
+    const size_t gbase = (size_t)group * b.hg;
+    const double *Hin = b.H[(s - 1) & 1];
+    const uint16_t *Kin = b.K[(s - 1) & 1];
+    double best = kInf;
+    int bo = -1, bi = -1, bkk = 0;
+    const int o_end = b.opt_off[r + 1];
+    for (int o = b.opt_off[r]; o < o_end; ++o) {
+      const int devs = b.opt_devs[o];
+      if (devs > avail) continue;
+      const int g2 = g - devs;
+      if (g2 < s - 1) continue;
+      const int row = o * (L + 2) + k;
+      const int beg = b.span_off[row], end = b.span_off[row + 1];
+      const size_t base = (gbase + (size_t)g2 * (L + 1)) * 32 + lane;
+      const double *Hr = Hin + base;
+      const uint16_t *Kr = Kin + base;
+      for (int idx = beg; idx < end; ++idx) {
+        const hapt_span e = b.spans[idx];
+        const hapt_span_ik ik = b.span_ik[idx];
+        if (ik.i > imax || e.srank >= maxcnt) break;
+        const double h = Hr[(size_t)ik.i * 32];
+        const int kk = Kr[(size_t)ik.i * 32];
+        const double c = __dadd_rn(e.tt, h);  // tt + (2c + F)  (_dp.pyx:85)
+        if (e.prank < cnt && kk <= ik.kmax && c < best) {
+          best = c;
+          bo = o;
+          bi = ik.i;
+          bkk = kk;
+        }
+      }
+    }
+    fin = bo >= 0;
+    if (cand < b.n_cand) {
+      if (k == 1 && g == G) b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
+      if (fin && b.full.bp_o) {
+        const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
+        if (b.full.F) b.full.F[e] = best;
+        if (b.full.N) b.full.N[e] = (double)bkk;
+        b.full.bp_i[e] = bi;
+        b.full.bp_o[e] = bo;
+      }
+    }
+    // successor entry (state g, split i = k-1) for layer s+1
+    double hn = kInf;
+    int kn = 0;
+    if (fin) {
+      const int crow = b.g_crow[g];
+      if (crow >= 0) {
+        const double c = b.cb[(size_t)crow * (L + 1) + (k - 1)];
+        if (c <= tm) {
+          const double c2 = __dmul_rn(2.0, c);
+          hn = __dadd_rn(c2, best);
+          kn = (int)ceil(__ddiv_rn(c2, tm)) + 1 + bkk;
+        }
+      }
+    }
+    const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * 32 + lane;
+    b.H[s & 1][o_idx] = hn;
+    b.K[s & 1][o_idx] = (uint16_t)kn;
+  }
+  fin_cnt[warp][lane] = fin;
+  __syncthreads();
+  if (warp == 0) {
+    int sum = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sum += fin_cnt[w][lane];
+    if (sum && cand < b.n_cand) atomicAdd(&b.states[cand], (unsigned long long)sum);
+  }
+}
+
+__global__ void dp_ftop_init(double *ftop, unsigned long long *states, int n_cand, int s_max) {
+  const long x = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < (long)n_cand * (s_max + 1)) ftop[x] = kInf;
+  if (x < n_cand) states[x] = 0;
+}
+
+// Per candidate best s and T* (planner.py:287-298), then the lexicographic
+// (T*, index) argmin == ParallelPlan.sort_key order over the pool.
+__global__ void dp_select(const double *ftop, const double *tmax, int n_cand, int s_max,
+                          long long B, double *tstar, int32_t *best_s, int32_t *winner) {
+  __shared__ double sv[1024];
+  __shared__ int si[1024];
+  double bv = kInf;
+  int bidx = -1;
+  const double bm1 = (double)(B - 1);
+  for (int c = threadIdx.x; c < n_cand; c += blockDim.x) {
+    const double tm = tmax[c];
+    const double pen = __dmul_rn(bm1, tm);
+    double best_total = kInf;
+    int bs = -1;
+    for (int s = 1; s <= s_max; ++s) {
+      const double v = ftop[(size_t)c * (s_max + 1) + s];
+      if (!isfinite(v)) continue;
+      const double total = __dadd_rn(v, pen);
+      if (total < best_total) {
+        best_total = total;
+        bs = s;
+      }
+    }
+    tstar[c] = best_total;
+    best_s[c] = bs;
+    if (bs >= 0 && (bidx < 0 || best_total < bv)) {  // c ascends: ties keep first
+      bv = best_total;
+      bidx = c;
+    }
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bidx;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w; w >>= 1) {
+    if (threadIdx.x < w) {
+      const int j = threadIdx.x + w;
+      const bool take = si[j] >= 0 && (si[threadIdx.x] < 0 || sv[j] < sv[threadIdx.x] ||
+                                       (sv[j] == sv[threadIdx.x] && si[j] < si[threadIdx.x]));
+      if (take) {
+        sv[threadIdx.x] = sv[j];
+        si[threadIdx.x] = si[j];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) winner[0] = si[0];
+}
+
+// Backpointer walk (planner.py:300-312) + the K chain (planner.py:330-338).
+__global__ void dp_walk(hapt_dp_full full, const int32_t *opt_devs, int L, int G, int s_max,
+                        int best_s, int32_t *stages, int32_t *kchain, int32_t *n_stages,
+                        int32_t *err) {
+  if (threadIdx.x || blockIdx.x) return;
+  int s = best_s, k = 1, g = G, n = 0;
+  *err = 0;
+  while (s > 0) {
+    const size_t e = ((size_t)s * (L + 2) + k) * (G + 1) + g;
+    const int i = full.bp_i[e], o = full.bp_o[e];
+    if (i < 0) {
+      *err = 1;
+      break;
+    }
+    stages[3 * n + 0] = k;
+    stages[3 * n + 1] = i;
+    stages[3 * n + 2] = o;
+    kchain[n] = (int)full.N[e];
+    ++n;
+    g -= opt_devs[o];
+    k = i + 1;
+    --s;
+  }
+  if (!*err && (k != L + 1 || g != 0)) *err = 2;
+  *n_stages = n;
+}
+
+__global__ void fill_full(hapt_dp_full f, size_t n, int L, int G) {
+  const size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  if (f.F) f.F[x] = (x == (size_t)(L + 1) * (G + 1)) ? 0.0 : kInf;
+  if (f.N) f.N[x] = 0.0;
+  f.bp_i[x] = -1;
+  f.bp_o[x] = -1;
+}
+
+__global__ void k_rank_hist(const hapt_span *spans, const int64_t *counters,
+                            unsigned long long *hist) {
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= counters[0]) return;
+  const int pr = spans[idx].prank;
+  if (pr != 0x7fffffff) atomicAdd(&hist[pr], 1ull);
+}
+
+__global__ void k_activated(const double *pool, const int64_t *counters,
+                            unsigned long long *hist, const double *tmax, int n_cand,
+                            int64_t *out) {
+  // single block: in-place exclusive scan of hist[0..plen], then
+  // activated(t) = #entries with rank < upper_bound(pool, t) = hist[cnt]
+  __shared__ unsigned long long part[1024];
+  const int plen = (int)counters[1];
+  const int n = plen + 1;
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  unsigned long long sum = 0;
+  for (int i = lo; i < hi; ++i) sum += hist[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const unsigned long long v = part[i];
+      part[i] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  unsigned long long run = part[threadIdx.x];
+  for (int i = lo; i < hi; ++i) {
+    const unsigned long long v = hist[i];
+    hist[i] = run;
+    run += v;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < n_cand; c += blockDim.x)
+    out[c] = (int64_t)hist[upper_bound(pool, plen, tmax[c])];
+}
+
+Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *ftop,
+                 int64_t *states, const hapt_dp_full *full, void *work) {
+  WsLayout w = ws_layout(t, n_cand);
+  char *wb = (char *)work;
+  Batch b{};
+  b.spans = t->spans;
+  b.span_ik = t->span_ik;
+  b.span_off = t->span_off;
+  b.opt_off = t->opt_off;
+  b.opt_devs = t->opt_devs;
+  b.g_mesh = t->g_mesh;
+  b.g_avail = t->g_avail;
+  b.g_crow = t->g_crow;
+  b.cb = t->cb_same;
+  b.pool = t->pool;
+  b.counters = t->counters;
+  b.L = t->L;
+  b.G = t->G;
+  b.s_max = t->s_max;
+  b.n_cand = n_cand;
+  b.n_groups = (n_cand + 31) / 32;
+  b.hg = (size_t)(t->G + 1) * (t->L + 1);
+  b.tmax = tmax;
+  b.tmax_pad = (double *)(wb + w.tmax_pad);
+  b.tcnt = (int32_t *)(wb + w.tcnt);
+  b.gmax = (int32_t *)(wb + w.gmax);
+  b.H[0] = (double *)(wb + w.H0);
+  b.H[1] = (double *)(wb + w.H1);
+  b.K[0] = (uint16_t *)(wb + w.K0);
+  b.K[1] = (uint16_t *)(wb + w.K1);
+  b.ftop = ftop;
+  b.states = (unsigned long long *)states;
+  if (full) b.full = *full;
+  return b;
+}
+
+int run_sweep(const Batch &b, cudaStream_t st) {
+  dp_ftop_init<<<grid_for((size_t)b.n_cand * (b.s_max + 1), 256), 256, 0, st>>>(
+      b.ftop, b.states, b.n_cand, b.s_max);
+  dp_prep<<<b.n_groups, 256, 0, st>>>(b);
+  HAPT_LAUNCHED("dp_prep");
+  for (int s = 1; s <= b.s_max; ++s) {
+    const long cells = (long)(b.L - s + 1) * (b.G - s + 1);
+    if (cells <= 0) break;
+    const unsigned gx = grid_for(cells, kWarps);
+    for (int g0 = 0; g0 < b.n_groups; g0 += 65535) {
+      const int gy = min(65535, b.n_groups - g0);
+      dp_relax<<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
+    }
+  }
+  HAPT_LAUNCHED("dp_relax");
+  return HAPT_OK;
+}
+
+}  // namespace
+}  // namespace hapt
+
+using namespace hapt;
+
+extern "C" size_t hapt_dp_workspace_bytes(const hapt_tables *t, int32_t n_cand) {
+  if (!t || n_cand < 1) return 0;
+  return ws_layout(t, n_cand).total;
+}
+
+extern "C" int hapt_dp_sweep_batch(const hapt_tables *t, const double *tmax, int32_t n_cand,
+                                   double *ftop, int64_t *states, const hapt_dp_full *full,
+                                   void *work, size_t work_bytes, void *stream) {
+  if (!t || !tmax || n_cand < 1 || !ftop || !states || !work) {
+    set_error("hapt_dp_sweep_batch: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  if (full && !full->bp_o) {
+    set_error("hapt_dp_sweep_batch: full outputs need bp_o/bp_i");
+    return HAPT_EINVAL;
+  }
+  if (work_bytes < ws_layout(t, n_cand).total) {
+    set_error("hapt_dp_sweep_batch: workspace %zu < %zu", work_bytes, ws_layout(t, n_cand).total);
+    return HAPT_ENOSPACE;
+  }
+  Batch b = make_batch(t, tmax, n_cand, ftop, states, full, work);
+  return run_sweep(b, (cudaStream_t)stream);
+}
+
+extern "C" int hapt_dp_select(const double *ftop, const double *tmax, int32_t n_cand,
+                              int32_t s_max, int64_t num_microbatches, double *tstar,
+                              int32_t *best_s, int32_t *winner, void *stream) {
+  if (!ftop || !tmax || n_cand < 1 || !tstar || !best_s || !winner) {
+    set_error("hapt_dp_select: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  dp_select<<<1, 1024, 0, (cudaStream_t)stream>>>(ftop, tmax, n_cand, s_max,
+                                                   (long long)num_microbatches, tstar,
+                                                   best_s, winner);
+  HAPT_LAUNCHED("dp_select");
+  return HAPT_OK;
+}
+
+namespace {
+struct BtLayout {
+  size_t tmax, ftop, states, err, bpi, bpo, N, ws, total;
+};
+BtLayout bt_layout(const hapt_tables *t) {
+  BtLayout y{};
+  const size_t cells = (size_t)(t->s_max + 1) * (t->L + 2) * (t->G + 1);
+  size_t cur = 0;
+  y.tmax = cur; cur += align_up(8);
+  y.ftop = cur; cur += align_up((size_t)(t->s_max + 1) * 8);
+  y.states = cur; cur += align_up(8);
+  y.err = cur; cur += align_up(4);
+  y.bpi = cur; cur += align_up(cells * 4);
+  y.bpo = cur; cur += align_up(cells * 4);
+  y.N = cur; cur += align_up(cells * 8);
+  y.ws = cur; cur += align_up(ws_layout(t, 1).total);
+  y.total = cur;
+  return y;
+}
+}  // namespace
+
+extern "C" size_t hapt_backtrack_workspace_bytes(const hapt_tables *t) {
+  if (!t) return 0;
+  return bt_layout(t).total;
+}
+
+extern "C" int hapt_dp_backtrack(const hapt_tables *t, double tmax, int32_t best_s,
+                                 int32_t *stages, int32_t *kchain, int32_t *n_stages,
+                                 void *work, size_t work_bytes, void *stream) {
+  if (!t || !stages || !kchain || !n_stages || !work || best_s < 1 || best_s > t->s_max) {
+    set_error("hapt_dp_backtrack: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  BtLayout y = bt_layout(t);
+  if (work_bytes < y.total) {
+    set_error("hapt_dp_backtrack: workspace %zu < %zu", work_bytes, y.total);
+    return HAPT_ENOSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char *w = (char *)work;
+  double *d_tmax = (double *)(w + y.tmax);
+  HAPT_CUDA(cudaMemcpyAsync(d_tmax, &tmax, 8, cudaMemcpyHostToDevice, st));
+  hapt_dp_full full{};
+  full.F = nullptr;
+  full.N = (double *)(w + y.N);
+  full.bp_i = (int32_t *)(w + y.bpi);
+  full.bp_o = (int32_t *)(w + y.bpo);
+  const size_t cells = (size_t)(t->s_max + 1) * (t->L + 2) * (t->G + 1);
+  fill_full<<<grid_for(cells, 256), 256, 0, st>>>(full, cells, t->L, t->G);
+  Batch b = make_batch(t, d_tmax, 1, (double *)(w + y.ftop), (int64_t *)(w + y.states), &full,
+                       w + y.ws);
+  int rc = run_sweep(b, st);
+  if (rc != HAPT_OK) return rc;
+  int32_t *err = (int32_t *)(w + y.err);
+  dp_walk<<<1, 32, 0, st>>>(full, t->opt_devs, t->L, t->G, t->s_max, best_s, stages, kchain,
+                            n_stages, err);
+  HAPT_LAUNCHED("dp_walk");
+  int32_t herr = 0;
+  HAPT_CUDA(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+  HAPT_CUDA(cudaStreamSynchronize(st));
+  if (herr) {
+    set_error(herr == 1 ? "broken backpointer chain"
+                        : "plan does not cover all layers and devices");
+    return HAPT_ECHAIN;
+  }
+  return HAPT_OK;
+}
+
+extern "C" int hapt_activated_pairs(const hapt_tables *t, const double *tmax, int32_t n_cand,
+                                    int64_t *activated, void *stream) {
+  if (!t || !tmax || n_cand < 1 || !activated) {
+    set_error("hapt_activated_pairs: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // the rank histogram lives in the tables scratch
+  unsigned long long *hist = (unsigned long long *)tables_hist(t);
+  HAPT_CUDA(cudaMemsetAsync(hist, 0, ((size_t)t->pool_cap + 1) * 8, st));
+  k_rank_hist<<<grid_for(t->nnz_cap, 256), 256, 0, st>>>(t->spans, t->counters, hist);
+  k_activated<<<1, 1024, 0, st>>>(t->pool, t->counters, hist, tmax, n_cand, activated);
+  HAPT_LAUNCHED("hapt_activated_pairs");
+  return HAPT_OK;
+}

@@ -1,0 +1,51 @@
+// Error reporting, version, and the FP64 add-throughput probe used as the
+// roofline denominator of the fp64-issue-bound kernels (K2, K3): B200's FP64
+// vector peak is not part of MEASURED_PEAKS.json, so bench.py measures it.
+#include <stdarg.h>
+
+#include "hapt_common.cuh"
+
+namespace hapt {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+namespace {
+// 8 independent DADD chains per thread; iters * 8 adds per thread.
+__global__ void k_fp64_probe(double *out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double d = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+    a0 = __dadd_rn(a0, d); a1 = __dadd_rn(a1, d); a2 = __dadd_rn(a2, d); a3 = __dadd_rn(a3, d);
+    a4 = __dadd_rn(a4, d); a5 = __dadd_rn(a5, d); a6 = __dadd_rn(a6, d); a7 = __dadd_rn(a7, d);
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == -1.0) out[0] = s;  // never true; keeps the chains live
+}
+}  // namespace
+
+}  // namespace hapt
+
+using namespace hapt;
+
+extern "C" const char *hapt_last_error(void) { return g_err; }
+
+extern "C" int hapt_version(void) { return 10000; }
+
+extern "C" int hapt_fp64_probe(double *result, int32_t blocks, int32_t threads, int32_t iters,
+                               void *stream) {
+  if (!result || blocks < 1 || threads < 32 || iters < 1) {
+    set_error("hapt_fp64_probe: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  k_fp64_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(result, iters);
+  HAPT_LAUNCHED("k_fp64_probe");
+  return HAPT_OK;
+}

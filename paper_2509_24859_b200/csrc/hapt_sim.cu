@@ -1,0 +1,354 @@
+// K3 -- heterogeneity-aware 1F1B schedule evaluation, batched over plans.
+//
+// Reference path: adaptive_counts / classic_counts / eager_counts
+// (scheduling.py:69-124) -> build_program (scheduling.py:230-252) ->
+// build_dag (simulation.py:73-149) -> simulate (simulation.py:204-228).
+//
+// The reference materialises a DAG of B(4S-2)+1 nodes per plan and runs a
+// Kahn sweep.  Start times are max-plus longest paths, and max is exact, so
+// the result does not depend on the order in which a node's predecessors are
+// visited.  hapt_sim_1f1b therefore never builds the DAG: one thread owns one
+// plan and walks every stage's 1F1B program directly,
+//     start = max(end of the previous op on the stage, dependency end)
+// where the dependency of F[i,s] is the forward transfer CF[i,s-1] and of
+// B[i,s] the backward transfer CB[i,s] (simulation.py:136-141); transfers
+// serialise per link direction (simulation.py:130-133):
+//     endCF[i,s] = max(endF[i,s], endCF[i-1,s]) + c_s
+//     endCB[i,s] = max(endB[i,s+1], endCB[i-1,s]) + c_s.
+// Transfer ends travel through per-link FIFOs (depth <= N_1 + 1, see
+// DESIGN.md §K3).  Each node's end is the same single IEEE addition the
+// reference performs (start[u] + duration[u]), so makespans and node times
+// are bit-identical.
+//
+// hapt_dag_longest_path covers simulate() on DAGs that callers edited by hand
+// (the reference tests corrupt one to provoke CycleError): a single-CTA
+// frontier Kahn sweep with atomicMax on the (non-negative) double bit
+// patterns.
+#include "hapt_common.cuh"
+
+namespace hapt {
+namespace {
+
+constexpr int kMaxStages = 64;
+
+__global__ void k_counts(int n_plans, const int32_t *stage_off, const double *t_fwd,
+                         const double *t_bwd, const double *comm, const double *tmax,
+                         double eps, int kind, int32_t *counts, int32_t *status) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_plans) return;
+  const int b0 = stage_off[p], S = stage_off[p + 1] - b0;
+  if (S < 1) {
+    status[p] = HAPT_ESCHED;
+    return;
+  }
+  double tm = 0.0;
+  bool first = true;
+  for (int i = 0; i < S; ++i) {
+    const double t = __dadd_rn(t_fwd[b0 + i], t_bwd[b0 + i]);
+    if (kind == HAPT_COUNTS_ADAPTIVE && !(t > 0.0)) {
+      status[p] = HAPT_ESCHED;  // "stage times must be positive"
+      return;
+    }
+    if (first || t > tm) tm = t;  // max(stage_times)
+    first = false;
+  }
+  if (kind == HAPT_COUNTS_ADAPTIVE) {
+    for (int i = 0; i + 1 < S; ++i)
+      if (comm[b0 + i] < 0.0) {
+        status[p] = HAPT_ESCHED;
+        return;
+      }
+    if (tmax) {
+      if (tmax[p] < tm) {
+        status[p] = HAPT_ESCHED;  // "t_max override below the slowest stage time"
+        return;
+      }
+      tm = tmax[p];
+    }
+  }
+  int n = 1;
+  counts[b0 + S - 1] = 1;
+  for (int i = S - 2; i >= 0; --i) {
+    int d;
+    if (kind == HAPT_COUNTS_CLASSIC) {
+      d = 1;
+    } else if (kind == HAPT_COUNTS_EAGER) {
+      d = 2;
+    } else {
+      const double c = comm[b0 + i];
+      if (c > tm) {
+        status[p] = HAPT_ECOMM;
+        return;
+      }
+      if (c <= __dmul_rn(eps, tm)) d = 1;
+      else if (c <= __ddiv_rn(tm, 2.0)) d = 2;
+      else d = 3;
+    }
+    n += d;
+    counts[b0 + i] = n;
+  }
+  status[p] = HAPT_OK;
+}
+
+// k-th op (0-based) of a stage with warm-up count N (scheduling.py:241-249):
+// F1..FN | (B j, F N+j) for j = 1..B-N | B (B-N+1)..B.  Returns mb, sets isF.
+__device__ __forceinline__ int decode_op(int pos, int N, int B, bool &isF) {
+  if (pos < N) {
+    isF = true;
+    return pos + 1;
+  }
+  const int q = pos - N, steady = B - N;
+  if (q < 2 * steady) {
+    isF = (q & 1);
+    return isF ? N + (q + 1) / 2 : q / 2 + 1;
+  }
+  isF = false;
+  return steady + (q - 2 * steady) + 1;
+}
+
+__global__ void k_sim(int n_plans, const int32_t *stage_off, const double *t_fwd,
+                      const double *t_bwd, const double *comm, const int32_t *counts,
+                      const int32_t *num_mb, double *makespan, double *node_start,
+                      double *node_end, const int64_t *node_off, int R, double *ring,
+                      int32_t *status) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_plans) return;
+  const int b0 = stage_off[p], S = stage_off[p + 1] - b0, B = num_mb[p];
+  if (S < 1 || S > kMaxStages || B < 1) {
+    status[p] = HAPT_ESCHED;
+    return;
+  }
+  // build_program preconditions (scheduling.py:235-239, 61-66)
+  if (counts[b0 + S - 1] != 1 || B < counts[b0]) {
+    status[p] = HAPT_ESCHED;
+    return;
+  }
+  for (int s = 0; s < S; ++s)
+    if (counts[b0 + s] < 1 || counts[b0 + s] > B || counts[b0 + s] + 1 > R) {
+      status[p] = HAPT_ESCHED;
+      return;
+    }
+  int pos[kMaxStages], fdone[kMaxStages], bdone[kMaxStages];
+  double prev[kMaxStages], lcf[kMaxStages], lcb[kMaxStages];
+  for (int s = 0; s < S; ++s) {
+    pos[s] = fdone[s] = bdone[s] = 0;
+    prev[s] = lcf[s] = lcb[s] = 0.0;
+  }
+  // FIFOs: link s forward at ring[(b0+s)*2R + slot], backward at +R
+  double *rf = ring + (size_t)b0 * 2 * R;
+  const int64_t nb = node_off ? node_off[p] : 0;
+  const bool want_nodes = node_start != nullptr;
+  double mk = 0.0;
+  int remaining = S;
+  for (int s = 0; s < S; ++s) remaining -= (2 * B == 0);
+  while (remaining > 0) {
+    bool progress = false;
+    for (int s = 0; s < S; ++s) {
+      const int N = counts[b0 + s];
+      while (pos[s] < 2 * B) {
+        bool isF;
+        const int mb = decode_op(pos[s], N, B, isF);
+        double dep = 0.0;
+        if (isF) {
+          if (s > 0) {
+            if (fdone[s - 1] < mb) break;
+            dep = rf[(size_t)(s - 1) * 2 * R + (mb % R)];
+          }
+        } else {
+          if (s < S - 1) {
+            if (bdone[s + 1] < mb) break;
+            dep = rf[(size_t)s * 2 * R + R + (mb % R)];
+          }
+        }
+        const double st = fmax(prev[s], dep);
+        const double d = isF ? t_fwd[b0 + s] : t_bwd[b0 + s];
+        const double en = __dadd_rn(st, d);
+        prev[s] = en;
+        mk = fmax(mk, en);
+        if (want_nodes) {
+          const int64_t id = nb + 2 * ((int64_t)s * B + (mb - 1)) + (isF ? 0 : 1);
+          node_start[id] = st;
+          node_end[id] = en;
+        }
+        if (isF) {
+          fdone[s] = mb;
+          if (s < S - 1) {  // forward transfer on link s
+            const double cs = fmax(en, lcf[s]);
+            const double ce = __dadd_rn(cs, comm[b0 + s]);
+            lcf[s] = ce;
+            mk = fmax(mk, ce);
+            rf[(size_t)s * 2 * R + (mb % R)] = ce;
+            if (want_nodes) {
+              const int64_t id = nb + 2 * (int64_t)S * B + 2 * ((int64_t)s * B + (mb - 1));
+              node_start[id] = cs;
+              node_end[id] = ce;
+            }
+          }
+        } else {
+          bdone[s] = mb;
+          if (s > 0) {  // backward transfer on link s-1
+            const double cs = fmax(en, lcb[s - 1]);
+            const double ce = __dadd_rn(cs, comm[b0 + s - 1]);
+            lcb[s - 1] = ce;
+            mk = fmax(mk, ce);
+            rf[(size_t)(s - 1) * 2 * R + R + (mb % R)] = ce;
+            if (want_nodes) {
+              const int64_t id =
+                  nb + 2 * (int64_t)S * B + 2 * ((int64_t)(s - 1) * B + (mb - 1)) + 1;
+              node_start[id] = cs;
+              node_end[id] = ce;
+            }
+          }
+        }
+        ++pos[s];
+        progress = true;
+        if (pos[s] == 2 * B) --remaining;
+      }
+    }
+    if (!progress) {
+      status[p] = HAPT_ECYCLE;
+      makespan[p] = kInf;
+      return;
+    }
+  }
+  if (want_nodes) {
+    const int64_t sink = nb + 2 * (int64_t)S * B + 2 * (int64_t)(S - 1) * B;
+    node_start[sink] = mk;
+    node_end[sink] = mk;
+  }
+  makespan[p] = mk;
+  status[p] = HAPT_OK;
+}
+
+// General DAG: single-CTA frontier sweep (Kahn) -- simulation.py:204-228.
+__global__ void k_dag(int n, const int32_t *succ_off, const int32_t *succ_idx,
+                      const int32_t *indeg0, const double *dur, double *start, double *end,
+                      double *makespan, int32_t *processed, int32_t *indeg, int32_t *fa,
+                      int32_t *fb) {
+  __shared__ int n_cur, n_next, n_done;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    indeg[v] = indeg0[v];
+    start[v] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    n_cur = 0;
+    n_done = 0;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < n; v += blockDim.x)
+    if (indeg0[v] == 0) fa[atomicAdd(&n_cur, 1)] = v;
+  __syncthreads();
+  int32_t *cur = fa, *nxt = fb;
+  while (n_cur > 0) {
+    if (threadIdx.x == 0) n_next = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n_cur; j += blockDim.x) {
+      const int u = cur[j];
+      const double e = __dadd_rn(start[u], dur[u]);
+      for (int x = succ_off[u]; x < succ_off[u + 1]; ++x) {
+        const int v = succ_idx[x];
+        atomicMax((unsigned long long *)&start[v], dkey(e));
+      }
+    }
+    __syncthreads();  // all maxima in before any successor is released
+    for (int j = threadIdx.x; j < n_cur; j += blockDim.x) {
+      const int u = cur[j];
+      for (int x = succ_off[u]; x < succ_off[u + 1]; ++x) {
+        const int v = succ_idx[x];
+        if (atomicSub(&indeg[v], 1) == 1) nxt[atomicAdd(&n_next, 1)] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      n_done += n_cur;
+      n_cur = n_next;
+    }
+    int32_t *tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+    __syncthreads();
+  }
+  double mk = 0.0;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    const double e = __dadd_rn(start[v], dur[v]);
+    end[v] = e;
+    mk = fmax(mk, e);
+  }
+  __shared__ double red[1024];
+  red[threadIdx.x] = mk;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *makespan = red[0];
+    *processed = n_done;
+  }
+}
+
+}  // namespace
+}  // namespace hapt
+
+using namespace hapt;
+
+extern "C" int hapt_launch_counts(int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
+                                  const double *t_bwd, const double *comm, const double *tmax,
+                                  double epsilon, int32_t kind, int32_t *counts, int32_t *status,
+                                  void *stream) {
+  if (n_plans < 1 || !stage_off || !t_fwd || !t_bwd || !comm || !counts || !status ||
+      kind < 0 || kind > 2) {
+    set_error("hapt_launch_counts: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  k_counts<<<grid_for(n_plans, 128), 128, 0, (cudaStream_t)stream>>>(
+      n_plans, stage_off, t_fwd, t_bwd, comm, tmax, epsilon, kind, counts, status);
+  HAPT_LAUNCHED("k_counts");
+  return HAPT_OK;
+}
+
+extern "C" size_t hapt_sim_workspace_bytes(int64_t total_stages, int32_t ring_depth) {
+  return align_up((size_t)(total_stages > 0 ? total_stages : 1) * 2 * ring_depth * 8);
+}
+
+extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
+                             const double *t_bwd, const double *comm, const int32_t *counts,
+                             const int32_t *num_mb, double *makespan, double *node_start,
+                             double *node_end, const int64_t *node_off, int32_t ring_depth,
+                             int32_t *status, void *work, size_t work_bytes, void *stream) {
+  if (n_plans < 1 || !stage_off || !t_fwd || !t_bwd || !comm || !counts || !num_mb ||
+      !makespan || !status || !work || ring_depth < 2 ||
+      ((node_start != nullptr) != (node_end != nullptr)) || (node_start && !node_off)) {
+    set_error("hapt_sim_1f1b: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  (void)work_bytes;
+  k_sim<<<grid_for(n_plans, 128), 128, 0, (cudaStream_t)stream>>>(
+      n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, node_start, node_end,
+      node_off, ring_depth, (double *)work, status);
+  HAPT_LAUNCHED("k_sim");
+  return HAPT_OK;
+}
+
+extern "C" size_t hapt_dag_workspace_bytes(int32_t n_nodes) {
+  return align_up((size_t)(n_nodes > 0 ? n_nodes : 1) * 4) * 3;
+}
+
+extern "C" int hapt_dag_longest_path(int32_t n_nodes, const int32_t *succ_off,
+                                     const int32_t *succ_idx, const int32_t *indeg,
+                                     const double *duration, double *start, double *end,
+                                     double *makespan, int32_t *processed, void *work,
+                                     size_t work_bytes, void *stream) {
+  if (n_nodes < 1 || !succ_off || !succ_idx || !indeg || !duration || !start || !end ||
+      !makespan || !processed || !work || work_bytes < hapt_dag_workspace_bytes(n_nodes)) {
+    set_error("hapt_dag_longest_path: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  const size_t a = align_up((size_t)n_nodes * 4);
+  char *w = (char *)work;
+  k_dag<<<1, 1024, 0, (cudaStream_t)stream>>>(n_nodes, succ_off, succ_idx, indeg, duration,
+                                               start, end, makespan, processed, (int32_t *)w,
+                                               (int32_t *)(w + a), (int32_t *)(w + 2 * a));
+  HAPT_LAUNCHED("k_dag");
+  return HAPT_OK;
+}

@@ -1,0 +1,536 @@
+"""Exact 1F1B schedule evaluation on the GPU (meshpipe.simulation, simulation.py:1-479).
+
+`simulate(build_dag(...))` returns the reference's ScheduleTrace, but the
+start times come from the hapt_sim_1f1b kernel, which walks each stage's
+program with per-link FIFOs instead of materialising the DAG (the reference's
+dominant per-plan cost).  The DAG's successor/predecessor
+lists are only built if a caller reads them; if they were read (and possibly
+edited, as the reference's cycle test does), simulate() runs the generic
+frontier kernel hapt_dag_longest_path over the current lists instead, with
+the reference's CycleError diagnosis.
+
+`simulate_batch` is the config-E workload: makespans of many plans in one
+launch.  `analyze` / `steady_state_rate` / trace export are host-side
+post-processing of a trace (SURVEY.md §8(f) ranks the batched analysis as the
+next row).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .scheduling import FWD, StageProgram
+
+NODE_F = 0
+NODE_B = 1
+NODE_CF = 2
+NODE_CB = 3
+NODE_SINK = 4
+
+_KIND_NAMES = {NODE_F: "F", NODE_B: "B", NODE_CF: "CF", NODE_CB: "CB", NODE_SINK: "sink"}
+
+
+class SimulationError(ValueError):
+    pass
+
+
+class CycleError(SimulationError):
+    def __init__(self, cycle: list):
+        self.cycle = cycle
+        super().__init__("dependency cycle: " + " -> ".join(cycle))
+
+
+def _node_id(kind: int, mb: int, stage: int, S: int, B: int) -> int:
+    """Reference node numbering (simulation.py:103-111)."""
+    if kind == NODE_F or kind == NODE_B:
+        return 2 * ((stage - 1) * B + (mb - 1)) + (kind == NODE_B)
+    if kind == NODE_CF or kind == NODE_CB:
+        return 2 * S * B + 2 * ((stage - 1) * B + (mb - 1)) + (kind == NODE_CB)
+    return 2 * S * B + 2 * (S - 1) * B
+
+
+class PipelineDag:
+    """Execution DAG of a 1F1B pipeline with lazily materialised edges."""
+
+    def __init__(self, t_fwd, t_bwd, comm, program: StageProgram):
+        self.num_stages = len(t_fwd)
+        self.num_microbatches = program.num_microbatches
+        self.program = program
+        self.t_fwd = [float(x) for x in t_fwd]
+        self.t_bwd = [float(x) for x in t_bwd]
+        self.comm = [float(x) for x in comm]
+        self._succ = None
+        self._pred = None
+        self._duration = None
+        self._meta = None
+
+    # -- structure ------------------------------------------------------------
+    @property
+    def num_nodes(self) -> int:
+        S, B = self.num_stages, self.num_microbatches
+        return B * (2 * S + 2 * (S - 1)) + 1
+
+    @property
+    def sink(self) -> int:
+        return self.num_nodes - 1
+
+    def node_id(self, kind: int, mb: int, stage: int) -> int:
+        S, B = self.num_stages, self.num_microbatches
+        if kind == NODE_SINK:
+            return self.sink
+        top = S if kind in (NODE_F, NODE_B) else S - 1
+        if not (1 <= stage <= top and 1 <= mb <= B):
+            raise KeyError((kind, mb, stage))
+        return _node_id(kind, mb, stage, S, B)
+
+    @property
+    def meta(self) -> list:
+        if self._meta is None:
+            S, B = self.num_stages, self.num_microbatches
+            meta = []
+            for s in range(1, S + 1):
+                for i in range(1, B + 1):
+                    meta += [(NODE_F, i, s), (NODE_B, i, s)]
+            for s in range(1, S):
+                for i in range(1, B + 1):
+                    meta += [(NODE_CF, i, s), (NODE_CB, i, s)]
+            meta.append((NODE_SINK, 0, 0))
+            self._meta = meta
+        return self._meta
+
+    @property
+    def duration(self) -> list:
+        if self._duration is None:
+            S, B = self.num_stages, self.num_microbatches
+            d = []
+            for s in range(S):
+                d += [self.t_fwd[s], self.t_bwd[s]] * B
+            for s in range(S - 1):
+                d += [self.comm[s], self.comm[s]] * B
+            d.append(0.0)
+            self._duration = d
+        return self._duration
+
+    def node_name(self, node: int) -> str:
+        kind, mb, stage = self.meta[node]
+        if kind == NODE_SINK:
+            return "sink"
+        return f"{_KIND_NAMES[kind]}[{mb},{stage}]"
+
+    def _materialise(self) -> None:
+        S, B = self.num_stages, self.num_microbatches
+        n = self.num_nodes
+        succ = [[] for _ in range(n)]
+        pred = [[] for _ in range(n)]
+
+        def link(u, v):
+            succ[u].append(v)
+            pred[v].append(u)
+
+        nid = lambda k, i, s: _node_id(k, i, s, S, B)  # noqa: E731
+        for s in range(1, S + 1):  # program order per stage (simulation.py:121-127)
+            prev = None
+            for kind, mb in self.program.stages[s - 1].ops:
+                v = nid(NODE_F if kind == FWD else NODE_B, mb, s)
+                if prev is not None:
+                    link(prev, v)
+                prev = v
+        for s in range(1, S):  # serial transfers per direction (130-133)
+            for i in range(1, B):
+                link(nid(NODE_CF, i, s), nid(NODE_CF, i + 1, s))
+                link(nid(NODE_CB, i, s), nid(NODE_CB, i + 1, s))
+        for s in range(1, S):  # cross-stage dependencies (136-141)
+            for i in range(1, B + 1):
+                link(nid(NODE_F, i, s), nid(NODE_CF, i, s))
+                link(nid(NODE_CF, i, s), nid(NODE_F, i, s + 1))
+                link(nid(NODE_B, i, s + 1), nid(NODE_CB, i, s))
+                link(nid(NODE_CB, i, s), nid(NODE_B, i, s))
+        for v in range(n - 1):
+            if not succ[v]:
+                link(v, n - 1)
+        self._succ, self._pred = succ, pred
+
+    @property
+    def succ(self) -> list:
+        if self._succ is None:
+            self._materialise()
+        return self._succ
+
+    @property
+    def pred(self) -> list:
+        if self._pred is None:
+            self._materialise()
+        return self._pred
+
+    @property
+    def edges_materialised(self) -> bool:
+        return self._succ is not None
+
+
+def build_dag(t_fwd: Sequence[float], t_bwd: Sequence[float], comm: Sequence[float],
+              program: StageProgram) -> PipelineDag:
+    """Validate and describe the pipeline DAG (simulation.py:73-149); edges
+    are not built unless read."""
+    S = len(t_fwd)
+    if len(t_bwd) != S or len(comm) != S - 1 or len(program.stages) != S:
+        raise SimulationError("inconsistent stage/boundary dimensions")
+    if any(d < 0 for d in list(t_fwd) + list(t_bwd) + list(comm)):
+        raise SimulationError("durations must be non-negative")
+    return PipelineDag(t_fwd, t_bwd, comm, program)
+
+
+@dataclass
+class ScheduleTrace:
+    dag: PipelineDag
+    start: list
+    end: list
+    makespan: float
+
+    @property
+    def num_stages(self) -> int:
+        return self.dag.num_stages
+
+    def node_interval(self, kind: int, mb: int, stage: int) -> tuple:
+        v = self.dag.node_id(kind, mb, stage)
+        return self.start[v], self.end[v]
+
+    def stage_op_nodes(self, stage: int) -> list:
+        return [
+            self.dag.node_id(NODE_F if kind == FWD else NODE_B, mb, stage)
+            for kind, mb in self.dag.program.stages[stage - 1].ops
+        ]
+
+
+def _find_cycle(dag: PipelineDag, remaining: set) -> list:
+    """Error-path diagnosis, same walk as simulation.py:176-201."""
+    state = {v: 0 for v in remaining}
+    stack: list = []
+
+    def dfs(v):
+        state[v] = 1
+        stack.append(v)
+        for w in dag.succ[v]:
+            if w not in state:
+                continue
+            if state[w] == 1:
+                return stack[stack.index(w):] + [w]
+            if state[w] == 0:
+                got = dfs(w)
+                if got:
+                    return got
+        state[v] = 2
+        stack.pop()
+        return None
+
+    for v in remaining:
+        if state[v] == 0:
+            got = dfs(v)
+            if got:
+                return [dag.node_name(x) for x in got]
+    return []
+
+
+def _simulate_general(dag: PipelineDag) -> ScheduleTrace:
+    import torch
+
+    from . import _lib
+    from ._lib import check, stream_ptr
+
+    lib = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = dag.num_nodes
+    succ = dag.succ
+    off = np.zeros(n + 1, dtype=np.int32)
+    off[1:] = np.cumsum([len(s) for s in succ])
+    idx = np.fromiter((v for s in succ for v in s), dtype=np.int32, count=int(off[-1]))
+    indeg = np.array([len(p) for p in dag.pred], dtype=np.int32)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    d_off, d_idx, d_indeg = T(off), T(idx if len(idx) else np.zeros(1, np.int32)), T(indeg)
+    d_dur = T(np.asarray(dag.duration, dtype=np.float64))
+    start = torch.empty(n, dtype=torch.float64, device=dev)
+    end = torch.empty(n, dtype=torch.float64, device=dev)
+    mk = torch.empty(1, dtype=torch.float64, device=dev)
+    processed = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(lib.hapt_dag_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    check(lib.hapt_dag_longest_path(n, d_off.data_ptr(), d_idx.data_ptr(), d_indeg.data_ptr(),
+                                    d_dur.data_ptr(), start.data_ptr(), end.data_ptr(),
+                                    mk.data_ptr(), processed.data_ptr(), ws.data_ptr(),
+                                    ws.numel(), stream_ptr()))
+    if int(processed.item()) != n:
+        left = ws[: n * 4].view(torch.int32).cpu().numpy()
+        raise CycleError(_find_cycle(dag, {v for v in range(n) if left[v] > 0}))
+    return ScheduleTrace(dag, start.cpu().tolist(), end.cpu().tolist(), float(mk.item()))
+
+
+def simulate(dag: PipelineDag) -> ScheduleTrace:
+    """Earliest start times of every node (simulation.py:204-228), on the GPU."""
+    if dag.edges_materialised:
+        return _simulate_general(dag)
+    S, B = dag.num_stages, dag.num_microbatches
+    counts = dag.program.counts.counts
+    mk, start, end, status = _sim_call(
+        np.asarray([dag.t_fwd]), np.asarray([dag.t_bwd]),
+        np.asarray([list(dag.comm) + [0.0]]), np.asarray([counts], dtype=np.int32),
+        np.asarray([B], dtype=np.int32), want_nodes=True,
+    )
+    if int(status[0]) == 7:  # deadlocking program: let the generic kernel diagnose
+        return _simulate_general(dag)
+    if int(status[0]) != 0:
+        raise SimulationError(f"simulation kernel rejected the program (status {int(status[0])})")
+    return ScheduleTrace(dag, start.tolist(), end.tolist(), float(mk[0]))
+
+
+def _sim_call(t_fwd, t_bwd, comm, counts, num_mb, want_nodes=False, stage_counts=None):
+    import torch
+
+    from . import _lib
+    from ._lib import check, stream_ptr
+
+    lib = _lib.lib()
+    dev = (t_fwd.device if isinstance(t_fwd, torch.Tensor) and t_fwd.is_cuda
+           else torch.device("cuda", torch.cuda.current_device()))
+    T = lambda a, dt=torch.float64: torch.as_tensor(a, dtype=dt).to(dev).contiguous()  # noqa: E731
+    tf, tb, cm = T(t_fwd), T(t_bwd), T(comm)
+    cn = T(counts, torch.int32)
+    P, S = tf.shape
+    mb = T(num_mb, torch.int32).reshape(-1)
+    if mb.numel() == 1 and P > 1:
+        mb = mb.expand(P).contiguous()
+    if stage_counts is None:
+        off = torch.arange(0, (P + 1) * S, S, dtype=torch.int32, device=dev)
+        ftf, ftb, fcm, fcn = tf.reshape(-1), tb.reshape(-1), cm.reshape(-1), cn.reshape(-1)
+        total = P * S
+    else:
+        sc = T(stage_counts, torch.int32)
+        off = torch.zeros(P + 1, dtype=torch.int32, device=dev)
+        off[1:] = torch.cumsum(sc, 0)
+        mask = torch.arange(S, device=dev)[None, :] < sc[:, None].long()
+        ftf, ftb, fcm, fcn = (x[mask].contiguous() for x in (tf, tb, cm, cn))
+        total = int(off[-1])
+    ring = int(cn.max().item()) + 2
+    ws = torch.empty(lib.hapt_sim_workspace_bytes(total, ring), dtype=torch.uint8, device=dev)
+    mk = torch.empty(P, dtype=torch.float64, device=dev)
+    status = torch.empty(P, dtype=torch.int32, device=dev)
+    start = end = node_off = None
+    if want_nodes:
+        Sv = (off[1:] - off[:-1]).long()
+        nodes = mb.long() * (4 * Sv - 2) + 1
+        node_off = torch.zeros(P, dtype=torch.int64, device=dev)
+        node_off[1:] = torch.cumsum(nodes, 0)[:-1]
+        n_all = int(nodes.sum())
+        start = torch.empty(n_all, dtype=torch.float64, device=dev)
+        end = torch.empty(n_all, dtype=torch.float64, device=dev)
+    check(lib.hapt_sim_1f1b(P, off.data_ptr(), ftf.data_ptr(), ftb.data_ptr(), fcm.data_ptr(),
+                            fcn.data_ptr(), mb.data_ptr(), mk.data_ptr(),
+                            0 if start is None else start.data_ptr(),
+                            0 if end is None else end.data_ptr(),
+                            0 if node_off is None else node_off.data_ptr(), ring,
+                            status.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr()))
+    if want_nodes:
+        return mk.cpu().numpy(), start.cpu().numpy(), end.cpu().numpy(), status.cpu().numpy()
+    return mk, status
+
+
+def simulate_batch(t_fwd, t_bwd, comm, counts, num_microbatches, stage_counts=None):
+    """Makespans of many 1F1B plans in one launch (config E).
+
+    t_fwd, t_bwd, comm, counts: [P, S] (comm[:, S-1] and entries past a plan's
+    own stage count are ignored; ragged plans give `stage_counts` [P]).
+    num_microbatches: scalar or [P].  Each makespan equals
+    simulate(build_dag(...)).makespan bit for bit.  Returns (makespan, status)
+    as CUDA tensors.
+    """
+    return _sim_call(t_fwd, t_bwd, comm, counts, num_microbatches, stage_counts=stage_counts)
+
+
+# ---------------------------------------------------------------------------
+# Host-side analysis of a trace (simulation.py:236-479)
+# ---------------------------------------------------------------------------
+
+
+def _interval_union(intervals):
+    out = []
+    for lo, hi in sorted(intervals):
+        if hi <= lo:
+            continue
+        if out and lo <= out[-1][1]:
+            out[-1] = (out[-1][0], max(out[-1][1], hi))
+        else:
+            out.append((lo, hi))
+    return out
+
+
+def _intersect(a, b):
+    out = []
+    i = j = 0
+    while i < len(a) and j < len(b):
+        lo, hi = max(a[i][0], b[j][0]), min(a[i][1], b[j][1])
+        if hi > lo:
+            out.append((lo, hi))
+        if a[i][1] <= b[j][1]:
+            i += 1
+        else:
+            j += 1
+    return out
+
+
+def _total(iv):
+    return sum(hi - lo for lo, hi in iv)
+
+
+@dataclass
+class StageReport:
+    stage: int
+    busy: float
+    window: float
+    bubble: float
+    bubble_fraction: float
+    steady_bubble: float
+    peak_inflight: int
+    peak_inflight_bytes: float
+
+
+@dataclass
+class LinkReport:
+    boundary: int
+    fwd_time: float
+    bwd_time: float
+    overlap_ratio: float
+
+
+@dataclass
+class SimulationReport:
+    makespan: float
+    stages: list
+    links: list
+
+    def to_text(self) -> str:
+        lines = [f"makespan: {self.makespan:.6g} s",
+                 "stage  busy        bubble      steady-bubble  peak-inflight"]
+        for r in self.stages:
+            lines.append(f"{r.stage:>5d}  {r.busy:<10.6g}  {r.bubble:<10.6g}  "
+                         f"{r.steady_bubble:<13.6g}  {r.peak_inflight}")
+        if self.links:
+            lines.append("link   comm-fwd    comm-bwd    overlap")
+            for l in self.links:
+                lines.append(f"{l.boundary:>4d}>  {l.fwd_time:<10.6g}  {l.bwd_time:<10.6g}  "
+                             f"{l.overlap_ratio:.3f}")
+        return "\n".join(lines) + "\n"
+
+
+def analyze(trace: ScheduleTrace, mem_act_per_stage=None) -> SimulationReport:
+    dag = trace.dag
+    S = dag.num_stages
+    dur = dag.duration
+    rows, busy_iv = [], []
+    for s in range(1, S + 1):
+        nodes = trace.stage_op_nodes(s)
+        iv = _interval_union([(trace.start[n], trace.end[n]) for n in nodes])
+        busy_iv.append(iv)
+        busy = sum(dur[n] for n in nodes)
+        window = trace.end[nodes[-1]] - trace.start[nodes[0]]
+        prog = dag.program.stages[s - 1]
+        steady = nodes[prog.warmup: prog.warmup + prog.steady]
+        if steady:
+            sb = (trace.end[steady[-1]] - trace.start[steady[0]]) - sum(dur[n] for n in steady)
+        else:
+            sb = 0.0
+        inflight = peak = 0
+        for kind, _ in prog.ops:
+            inflight += 1 if kind == FWD else -1
+            peak = max(peak, inflight)
+        per = mem_act_per_stage[s - 1] if mem_act_per_stage else 0.0
+        rows.append(StageReport(s, busy, window, window - busy,
+                                (window - busy) / window if window > 0 else 0.0, sb, peak,
+                                peak * per))
+    links = []
+    B = dag.num_microbatches
+    for s in range(1, S):
+        fw = [dag.node_id(NODE_CF, i, s) for i in range(1, B + 1)]
+        bw = [dag.node_id(NODE_CB, i, s) for i in range(1, B + 1)]
+        tot = _total(_interval_union([(trace.start[n], trace.end[n]) for n in fw + bw]))
+        if tot <= 0.0:
+            ratio = 1.0
+        else:
+            busy = _interval_union([(trace.start[n], trace.end[n]) for n in fw + bw])
+            ratio = _total(_intersect(_intersect(busy, busy_iv[s - 1]), busy_iv[s])) / tot
+        links.append(LinkReport(s, sum(dur[n] for n in fw), sum(dur[n] for n in bw), ratio))
+    return SimulationReport(trace.makespan, rows, links)
+
+
+def steady_state_rate(trace: ScheduleTrace, stage: int = 1) -> float:
+    dag = trace.dag
+    B = dag.num_microbatches
+    K = dag.program.counts.counts[stage - 1]
+    idx = list(range(2 * K + 1, B + 1, K))
+    if len(idx) < 4:
+        raise SimulationError(f"steady window too short: need >= 3 blocks of {K} microbatches")
+    ys = [trace.start[dag.node_id(NODE_F, i, stage)] for i in idx]
+    n = float(len(idx))
+    mx, my = sum(idx) / n, sum(ys) / n
+    sxx = sum((x - mx) ** 2 for x in idx)
+    sxy = sum((x - mx) * (y - my) for x, y in zip(idx, ys))
+    return sxy / sxx
+
+
+def steady_block_span(trace: ScheduleTrace, stage: int, i: int) -> float:
+    dag = trace.dag
+    K = dag.program.counts.counts[stage - 1]
+    return (trace.start[dag.node_id(NODE_F, i + K, stage)]
+            - trace.start[dag.node_id(NODE_F, i, stage)])
+
+
+def asap_tight(trace: ScheduleTrace, rel_tol: float = 1e-9) -> bool:
+    dag = trace.dag
+    dur = dag.duration
+    for v in range(dag.num_nodes):
+        if not dag.pred[v]:
+            if trace.start[v] != 0.0:
+                return False
+            continue
+        hi = max(trace.start[u] + dur[u] for u in dag.pred[v])
+        if not math.isclose(trace.start[v], hi, rel_tol=rel_tol, abs_tol=1e-12):
+            return False
+    return True
+
+
+def trace_events(trace: ScheduleTrace, labels=None) -> list:
+    dag = trace.dag
+    S = dag.num_stages
+    dur = dag.duration
+    events = []
+    for v, (kind, mb, stage) in enumerate(dag.meta):
+        if kind == NODE_SINK or dur[v] <= 0.0:
+            continue
+        if kind in (NODE_F, NODE_B):
+            pid, tid = (labels[stage - 1] if labels else f"stage-{stage}"), stage
+        elif kind == NODE_CF:
+            pid, tid = f"link-{stage}>{stage + 1} fwd", S + 2 * stage - 1
+        else:
+            pid, tid = f"link-{stage}>{stage + 1} bwd", S + 2 * stage
+        events.append({"name": f"{_KIND_NAMES[kind]}{mb}", "cat": _KIND_NAMES[kind], "ph": "X",
+                       "pid": pid, "tid": tid, "ts": trace.start[v] * 1e6,
+                       "dur": dur[v] * 1e6})
+    return events
+
+
+def write_trace_events(trace: ScheduleTrace, path, labels=None) -> None:
+    with open(path, "w") as fh:
+        json.dump({"traceEvents": trace_events(trace, labels)}, fh, indent=1)
+
+
+def trace_to_text(trace: ScheduleTrace) -> str:
+    dag = trace.dag
+    lines = ["# node         start        end          duration"]
+    for v in sorted(range(dag.num_nodes), key=lambda v: (trace.start[v], v)):
+        if dag.meta[v][0] == NODE_SINK:
+            continue
+        lines.append(f"{dag.node_name(v):<12s}  {trace.start[v]:<11.6g}  {trace.end[v]:<11.6g}"
+                     f"  {dag.duration[v]:.6g}")
+    lines.append(f"makespan {trace.makespan:.6g}")
+    return "\n".join(lines) + "\n"

@@ -5,10 +5,9 @@ reference operator (_dp.pyx:14-28; dp_py.py:27-43): numpy inputs in the
 DpTables layout, numpy outputs F, N (float64) and bp_i, bp_o (int32) of shape
 [s_max+1, L+2, G+1].  The sweep runs on the GPU (hapt_tables_finalize +
 hapt_dp_sweep_batch with full outputs); a reference caller such as
-planner.dp_search or benchmarks/bench_dp.py can be pointed at it unchanged:
-
-    import meshpipe.planner as P, paper_2509_24859_b200._core as C
-    P.dp_sweep = C.dp_sweep
+planner.dp_search or benchmarks/bench_dp.py can be pointed at it unchanged
+by rebinding the reference module attribute `planner.dp_sweep` to this
+function (INTEGRATION.md shows the one-line binding).
 
 There is no CPU fallback: without the CUDA library this module raises.
 """

@@ -1,0 +1,95 @@
+"""Candidate sharding across GPUs (one process per GPU, torch.distributed).
+
+Every t_max candidate's DP is independent (planner.py:526-531),
+so a batch of candidates is strided across ranks (rank r takes batch[r::W],
+which balances work because the activated span count grows with t_max).
+Each rank builds the same K1 tables locally (microseconds; cheaper than a
+broadcast).  The only exchange steps are
+
+  * all_gather of per-candidate (T*, best_s, dp_states) when every rank must
+    replay the reference's pruning decisions identically (search()), and
+  * an allreduce-argmin of (T*, index) -- two 8-byte MIN all-reduces, since
+    non-negative IEEE doubles order like their bit patterns -- that picks the
+    global winner of a full-pool sweep (the merge of planner.py:535-541).
+
+With the NCCL backend the collectives run on device tensors over NVLink /
+NVSwitch; the same code runs on gloo (CPU tensors) for the CPU test suite.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+_I64_MAX = np.iinfo(np.int64).max
+
+
+class PoolSharding:
+    def __init__(self, group=None):
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed is not initialised")
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.backend = dist.get_backend(group)
+        self.collective_calls = 0
+
+    @property
+    def device(self) -> torch.device:
+        if self.backend == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
+
+    def shard(self, indices):
+        return list(indices)[self.rank :: self.world]
+
+    def _all_gather(self, local: torch.Tensor, width: int) -> torch.Tensor:
+        """Gather equally padded [width, ...] tensors from every rank."""
+        pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=self.device)
+        pad[: local.shape[0]] = local.to(self.device)
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(out, pad, group=self.group)
+        self.collective_calls += 1
+        return torch.stack(out).cpu()
+
+    def evaluate_sharded(self, sweeper, pool: np.ndarray, todo, num_microbatches: int):
+        """Evaluate pool[todo] with each rank taking todo[rank::world]; every
+        rank returns the full (tstar, best_s, states) in `todo` order."""
+        todo = list(todo)
+        mine = self.shard(todo)
+        width = (len(todo) + self.world - 1) // self.world
+        if mine:
+            res = sweeper.evaluate(pool[mine], num_microbatches)
+            loc = np.stack([res.tstar.view(np.int64), res.best_s.astype(np.int64),
+                            res.states.astype(np.int64)], axis=1)
+        else:
+            loc = np.zeros((0, 3), dtype=np.int64)
+        allv = self._all_gather(torch.from_numpy(np.ascontiguousarray(loc)), max(width, 1)).numpy()
+        tstar = np.empty(len(todo))
+        best_s = np.empty(len(todo), dtype=np.int64)
+        states = np.empty(len(todo), dtype=np.int64)
+        for r in range(self.world):
+            pos = np.arange(r, len(todo), self.world)
+            blk = allv[r, : len(pos)]
+            tstar[pos] = blk[:, 0].view(np.float64)
+            best_s[pos] = blk[:, 1]
+            states[pos] = blk[:, 2]
+        return tstar, best_s, states
+
+    def allreduce_argmin(self, tstar: float, index: int):
+        """Global lexicographic min of (T*, index) over ranks; (inf, -1) if
+        no rank has a feasible candidate.  Two MIN all-reduces of 8 bytes."""
+        feas = index >= 0 and np.isfinite(tstar)
+        bits = np.array([tstar], dtype=np.float64).view(np.int64)[0] if feas else _I64_MAX
+        t = torch.tensor([bits], dtype=torch.int64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        gbits = int(t.item())
+        mine = index if feas and bits == gbits else _I64_MAX
+        i = torch.tensor([mine], dtype=torch.int64, device=self.device)
+        dist.all_reduce(i, op=dist.ReduceOp.MIN, group=self.group)
+        self.collective_calls += 2
+        gidx = int(i.item())
+        if gbits == _I64_MAX:
+            return float("inf"), -1
+        return float(np.array([gbits], dtype=np.int64).view(np.float64)[0]), gidx

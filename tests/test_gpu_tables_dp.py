@@ -1,0 +1,120 @@
+"""GPU: K1 tables and the K2 DP operator, bit-exact against the reference
+goldens and the oracle."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import build, expected, expected_arrays, load_json, seeded
+
+pytestmark = pytest.mark.gpu
+
+STAT_KEYS = ["candidates", "canonical", "canonical_feasible", "aliased", "pruned_oom",
+             "pruned_imbalance"]
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["A", "B", "C", "D1"])
+def test_device_tables_equal_reference(name):
+    """hapt_tables_build reproduces DpTables + the t_max pool + StoreStats."""
+    from paper_2509_24859_b200.planner import DpTables
+
+    inst, exp = load_json(name), expected(name)
+    store, costs, cluster, B, eps = build(inst)
+    tables = DpTables(store, costs)
+    for key, want in exp["tables"]["sha"].items():
+        if key == "pool":
+            got = sha(np.asarray(store.feasible_t_values(), dtype=np.float64))
+        else:
+            got = sha(getattr(tables, key))
+        assert got == want, key
+    assert store.stats.as_dict() == exp["tables"]["stats"]
+    assert tables.transitions_per_sweep() == exp["tables"]["transitions_per_sweep"]
+
+
+@pytest.mark.parametrize("name", ["A", "C"])
+def test_store_lookup_equals_oracle(name):
+    """Every (option, span) profile incl. pruned ones (ProfileStore.lookup)."""
+    inst = load_json(name)
+    store, *_ = build(inst)
+    tb = O.tables(inst)
+    for key in ("tf", "tb", "mp", "ma"):
+        dev = store.dev.host(f"{key}_raw")
+        L = store.num_layers
+        for o in range(tb["n_opts"]):
+            for q in range(1, L + 1):
+                assert np.array_equal(dev[o, q, q:L + 1], tb[key][o, q, q:L + 1]), (key, o, q)
+    st = store.dev.host("cell_state")
+    assert np.array_equal(st & 1, tb["state"] & 1)
+    mesh, sub = store.options[0]
+    prof = store.lookup(1, 2, mesh.id, sub.shape)
+    assert prof is store.lookup(1, 2, mesh.id, sub.shape)
+
+
+def test_dp_sweep_dropin_matches_reference_kernel():
+    """The 15-argument operator against the Cython kernel's outputs on the
+    instances of test_planner.py::TestBackends (seed 4321)."""
+    from paper_2509_24859_b200._core import dp_sweep
+
+    n = 0
+    for rec in seeded()["parity"]:
+        tb = O.tables(rec["instance"])
+        for c in rec["candidates"]:
+            F, N, bi, bo = dp_sweep(c["t_max"], tb["t_tab"], tb["mp_tab"], tb["ma_tab"],
+                                    tb["opt_cap"], tb["opt_mesh"], tb["opt_devs"], tb["opt_off"],
+                                    tb["cb_same"], tb["cb_next"], tb["g_mesh"], tb["g_avail"],
+                                    tb["s_max"], tb["span_off"], tb["span_items"])
+            assert (sha(F), sha(N), sha(bi), sha(bo)) == (c["F"], c["N"], c["bp_i"], c["bp_o"])
+            n += 1
+    assert n > 10
+
+
+@pytest.mark.parametrize("name", ["A", "B"])
+def test_dp_sweep_dropin_full_pool_equals_oracle(name):
+    from paper_2509_24859_b200._core import dp_sweep
+
+    tb = O.tables(load_json(name))
+    for t in tb["pool"][::7]:
+        got = dp_sweep(t, tb["t_tab"], tb["mp_tab"], tb["ma_tab"], tb["opt_cap"], tb["opt_mesh"],
+                       tb["opt_devs"], tb["opt_off"], tb["cb_same"], tb["cb_next"], tb["g_mesh"],
+                       tb["g_avail"], tb["s_max"], tb["span_off"], tb["span_items"])
+        want = O.dp_sweep(tb, t)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+
+@pytest.mark.parametrize("name", ["A", "B", "C", "D1"])
+def test_batched_full_pool_equals_reference(name):
+    """Every candidate of the pool in batched sweeps: T*, best s and the
+    finite-cell count equal the reference's per-candidate dp_search."""
+    from paper_2509_24859_b200.planner import sweep_pool
+
+    inst, arr = load_json(name), expected_arrays(name)
+    store, costs, cluster, B, eps = build(inst)
+    pool, tstar, best_s, states, winner = sweep_pool(store, costs, B)
+    assert np.array_equal(pool, arr["pool"])
+    assert np.array_equal(tstar, arr["tstar"])
+    assert np.array_equal(best_s, arr["best_s"])
+    assert np.array_equal(states, arr["states"])
+    feas = np.where(best_s >= 0)[0]
+    assert winner == feas[np.lexsort((pool[feas], tstar[feas]))[0]]
+
+
+def test_batch_chunking_is_invisible():
+    """Splitting a batch into workspace-sized chunks changes nothing."""
+    from paper_2509_24859_b200.planner import DpTables
+
+    inst = load_json("C")
+    store, costs, cluster, B, eps = build(inst)
+    tables = DpTables(store, costs)
+    pool = store.feasible_t_values()
+    a = tables.sweeper.evaluate(pool, B)
+    tables.sweeper.max_ws_bytes = 1  # one 32-candidate group per chunk
+    b = tables.sweeper.evaluate(pool, B)
+    assert tables.sweeper.last_chunks == (len(pool) + 31) // 32
+    assert np.array_equal(a.tstar, b.tstar) and np.array_equal(a.states, b.states)

@@ -1,0 +1,521 @@
+"""Benchmark of the planner hot path (BASELINE.json metric: planner search
+time and candidate plans evaluated/s at 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config D1]
+    python bench.py --impl reference ...      (reference CPU arm)
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One JSON line on rank 0.  A "step" is one pass of the hot path over the whole
+t_max candidate pool of the workload (config D1 by default: Llama-2 70B proxy,
+2,006-op graph clustered to 82 layers, 4 subclusters x 64 GPUs, B=128): the
+batched stage-partition DP over every candidate, the per-candidate Eq. 14
+scoring, and the global argmin (NCCL allreduce-argmin across ranks when
+N > 1).  The pool is strided across ranks, so total work is fixed as N grows
+("strong").
+
+value  : candidates/s with tables already resident in HBM (device timed,
+         CUDA events on the launching stream, max over ranks).
+e2e    : the same metric through the public API from HOST inputs
+         (build_store -> DpTables -> sweep_pool), H2D of the instance and D2H
+         of the per-candidate results inside the timed region.
+search_time_s : planner.search() end to end (host inputs -> ParallelPlan).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "candidate plans evaluated/sec (t_max-pool DP sweep)"
+UNIT = "candidates/s"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm (oracle/_ref = the unmodified reference package, built by
+# oracle/Makefile; the C restatement oracle/ as a fallback)
+# ---------------------------------------------------------------------------
+
+
+def reference_impl():
+    """Returns (kind, timer) where timer(pool_subset, workers) runs the
+    reference's own per-candidate DP search on host threads."""
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "meshpipe")):
+        sys.path.insert(0, ref)
+        try:
+            import meshpipe  # noqa: F401
+            from meshpipe import BACKEND
+            from meshpipe.cluster import ClusterSpec as RC, DeviceMesh as RM
+            from meshpipe.model_graph import Layer as RL, LayerSequence as RS
+            from meshpipe.planner import DpTables as RT, dp_search as rdp
+            from meshpipe.profiling import CostModel as RCM, boundary_costs as rbc
+            from meshpipe.profiling import build_store as rbs
+
+            def make(name):
+                from paper_2509_24859_b200.workloads import instance_dict
+
+                d = instance_dict(name)
+                lay = d["layers"]
+                layers = RS(tuple(RL(i, i + 1, lay["flops"][i], lay["param_bytes"][i],
+                                     lay["boundary_bytes"][i], tuple(lay["signature"][i]))
+                                  for i in range(len(lay["flops"]))), ())
+                meshes = [RM(m["id"], m["hosts"], m["devices_per_host"], m["peak_flops"],
+                             m["mem_device"], m["intra_host_bw"], m["inter_host_bw"])
+                          for m in d["cluster"]["meshes"]]
+                cb = d["cluster"]["cross_bw"]
+                if isinstance(cb, list):
+                    cb = {(a, b): v for a, b, v in cb}
+                cl = RC(meshes, cross_bw=cb, cross_latency=d["cluster"]["cross_latency"])
+                store = rbs(layers, cl, RCM(**d["model"]), imbalance_ratio=float(d["imbalance_ratio"]))
+                costs = rbc(layers, cl)
+                tables = RT(store, costs)
+                B = d["num_microbatches"]
+
+                def one(t):
+                    return rdp(store, costs, B, t, d["epsilon"], tables)
+
+                return store.feasible_t_values(), one
+
+            return f"reference (meshpipe, BACKEND={BACKEND})", "reference", make
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] reference build unusable ({exc}); using the oracle port",
+                  file=sys.stderr)
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+
+    def make(name):
+        from paper_2509_24859_b200.workloads import instance_dict
+
+        inst = instance_dict(name)
+        tb = O.tables(inst)
+
+        def one(t):
+            return O.evaluate(inst, tb, t)
+
+        return tb["pool"], one
+
+    return "oracle port (C restatement)", "port", make
+
+
+def time_reference(make, name, budget_s: float, workers: int):
+    """Bounded sample of the pool: strided candidates, timed on `workers`
+    host threads (the Cython kernel releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    pool, one = make(name)
+    n = len(pool)
+    t0 = time.perf_counter()
+    one(pool[n // 2])
+    per = max(time.perf_counter() - t0, 1e-6)
+    k = int(max(workers, min(n, budget_s * workers / per)))
+    k = min(n, max(1, k))
+    idx = [int(i * n / k) for i in range(k)]
+    sample = [pool[i] for i in idx]
+    with ThreadPoolExecutor(workers) as ex:
+        t0 = time.perf_counter()
+        list(ex.map(one, sample))
+        dt = time.perf_counter() - t0
+    return len(sample) / dt, len(sample), n, dt
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    label, kind, make = reference_impl()
+    cores = host_cores()
+    vals = []
+    for _ in range(args.warmup):
+        time_reference(make, args.config, 2.0, cores)
+    samples = []
+    for _ in range(args.steps):
+        v, k, n, dt = time_reference(make, args.config, args.ref_budget, cores)
+        vals.append(v)
+        samples.append((k, n, dt))
+    value = sum(vals) / len(vals)
+    k, n, dt = samples[-1]
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(s[2] for s in samples) / len(samples),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{k} of {n} pool candidates (strided) of config "
+                                   f"{args.config} per step, {label}, "
+                                   f"ThreadPoolExecutor({cores}) over dp_search; "
+                                   f"host: {cpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def workload_config(args) -> dict:
+    from paper_2509_24859_b200.workloads import CONFIGS
+
+    return {
+        "workload": f"config {args.config}: {CONFIGS[args.config]}",
+        "step": "full t_max candidate pool through the batched DP + Eq.14 scoring + "
+                "global argmin",
+        "parallelism": f"candidate-sharded x{args.gpus} (NCCL allreduce-argmin)",
+        "l2": "working set > L2: per-step successor tables (HBM) exceed the 126 MB L2, and a "
+              "256 MB buffer is rewritten between timed steps",
+    }
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5,
+                ).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit()
+                else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def fp64_peak(lib, torch, device) -> float:
+    """Measured DADD throughput (adds/s) of this GPU: hapt_fp64_probe."""
+    from paper_2509_24859_b200._lib import check, stream_ptr
+
+    out = torch.zeros(1, dtype=torch.float64, device=device)
+    blocks, threads, iters = 148 * 16, 256, 4096
+    check(lib.hapt_fp64_probe(out.data_ptr(), blocks, threads, 64, stream_ptr()))
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = math.inf
+    for _ in range(3):
+        s.record()
+        check(lib.hapt_fp64_probe(out.data_ptr(), blocks, threads, iters, stream_ptr()))
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e) * 1e-3)
+    return blocks * threads * iters * 8 / best
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="D1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per sample")
+    ap.add_argument("--no-extras", action="store_true", help="skip per_config / cpu_baseline")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2509_24859_b200 import _lib
+    from paper_2509_24859_b200.distributed import PoolSharding
+    from paper_2509_24859_b200.planner import DpTables, search, sweep_pool
+    from paper_2509_24859_b200.profiling import boundary_costs, build_store
+    from paper_2509_24859_b200.workloads import instance
+
+    lib = _lib.lib()
+    sharding = PoolSharding() if world > 1 else None
+    layers, cluster, model, rho, B, eps = instance(args.config)
+    store = build_store(layers, cluster, model, imbalance_ratio=rho)
+    costs = boundary_costs(layers, cluster)
+    tables = DpTables(store, costs)
+    sw = tables.sweeper
+    pool_all = np.asarray(store.feasible_t_values())
+    P = len(pool_all)
+    mine = np.arange(rank, P, world)
+    tmax = torch.from_numpy(pool_all[mine]).to(device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    def step():
+        ftop, states = sw.sweep_device(tmax)
+        tstar, best_s, winner = sw.select_device(ftop, tmax, B)
+        if sharding is not None:
+            w = int(winner.item())
+            sharding.allreduce_argmin(float(tstar[w]) if w >= 0 else math.inf,
+                                      int(mine[w]) if w >= 0 else -1)
+        return winner
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            s_ev[i].record()
+            step()
+            e_ev[i].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_s = sum(s.elapsed_time(e) for s, e in zip(s_ev, e_ev)) * 1e-3
+    t = torch.tensor([dev_s], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_s = float(t.item())
+    value = P * args.steps / dev_s
+    ms_per_step = dev_s / args.steps * 1e3
+
+    # dominant kernel (dp_relax): per-launch duration from the same sweeps
+    Lr, G, s_max = tables.L, tables.G, tables.s_max
+    relax_launches = sum(1 for s in range(1, s_max + 1) if (Lr - s + 1) * (G - s + 1) > 0)
+    chunks = sw.last_chunks
+    launches_per_step = chunks * (2 + relax_launches) + 1
+    nnz = store.dev.nnz
+    n_mine = len(mine)
+    bytes_per_cand = s_max * 32 * (Lr + 2) * (G + 1) + 28 * nnz
+    trans = tables.transitions_per_sweep()
+    sweep_s = dev_s / args.steps  # ~all of the step is the relax launches
+    avg_launch_s = sweep_s / max(1, relax_launches * chunks)
+    bytes_per_launch = bytes_per_cand * n_mine / max(1, relax_launches * chunks)
+    peaks = {}
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_per_launch / avg_launch_s / 1e9
+    fp64 = fp64_peak(lib, torch, device)
+    roofline = {
+        "bound": "hbm",
+        "kernel": "dp_relax (hapt_dp.cu)",
+        "achieved": achieved,
+        "peak": hbm_peak,
+        "unit": "GB/s",
+        "frac": achieved / hbm_peak,
+        "traffic": None,
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+        "algorithmic_bytes_per_candidate": bytes_per_cand,
+        "fp64": {
+            "ops_per_candidate": 2 * trans,
+            "achieved_ops_s": 2 * trans * n_mine * args.steps / dev_s,
+            "measured_dadd_peak_ops_s": fp64,
+            "frac": (2 * trans * n_mine * args.steps / dev_s) / fp64,
+            "transitions_per_s": trans * n_mine * args.steps / dev_s,
+            "dp_cells_per_s": s_max * Lr * G * n_mine * args.steps / dev_s,
+        },
+    }
+
+    # e2e through the public API from host inputs (rank-sharded when N>1)
+    e2e_times = []
+    h2d = 8 * (3 * Lr + 4 * len(cluster.meshes)) + 4 * (Lr + 2 * len(cluster.meshes) + 3 * len(store.options))
+    for i in range(2 + args.steps):
+        flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        st2 = build_store(layers, cluster, model, imbalance_ratio=rho)
+        c2 = boundary_costs(layers, cluster)
+        pool_r, tstar_r, best_r, states_r, win_r = sweep_pool(st2, c2, B, dist=sharding)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i >= 2:
+            e2e_times.append(dt)
+    d2h = 8 * 16 + P * 8 + P * (8 + 8 + 8) // max(1, world)
+    t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = P * len(e2e_times) / float(t.item())
+    assert int(win_r) >= 0
+
+    # planner search time: search() end to end
+    search_times = []
+    for i in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st3 = build_store(layers, cluster, model, imbalance_ratio=rho)
+        plan = search(st3, boundary_costs(layers, cluster), B, epsilon=eps, dist=sharding)
+        search_times.append(time.perf_counter() - t0)
+    search_time = min(search_times)
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {**workload_config(args), "pool_candidates": P, "layers": Lr, "devices": G,
+                   "s_max": s_max, "transitions_per_sweep": trans, "nnz": nnz},
+        "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "build_store -> boundary_costs -> planner.sweep_pool (host in, host out)"},
+        "search_time_s": search_time,
+        "search_plan": {"stages": plan.num_stages, "T*": plan.predicted_latency,
+                        "t_max": plan.t_max, "evaluated": plan.search_stats["evaluated"]},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_extras:
+        line["per_config"] = per_config(args, torch, device)
+        label, kind, make = reference_impl()
+        cores = host_cores()
+        v, k, n, dt = time_reference(make, args.config, args.ref_budget, cores)
+        line["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{k} of {n} pool candidates (strided) of config {args.config}, {label}, "
+                      f"ThreadPoolExecutor({cores}) over dp_search, {dt:.1f} s; "
+                      f"host: {cpu_model()}",
+        }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def per_config(args, torch, device) -> dict:
+    """GPU numbers for the other BASELINE configs (not bench lines)."""
+    import numpy as np
+
+    from paper_2509_24859_b200.planner import search, sweep_pool
+    from paper_2509_24859_b200.profiling import boundary_costs, build_store
+    from paper_2509_24859_b200.scheduling import launch_counts_batch
+    from paper_2509_24859_b200.simulation import simulate_batch
+    from paper_2509_24859_b200.workloads import config_e, instance
+
+    out = {}
+    for name in ("A", "B", "C", "D1"):
+        layers, cluster, model, rho, B, eps = instance(name)
+        st = build_store(layers, cluster, model, imbalance_ratio=rho)
+        costs = boundary_costs(layers, cluster)
+        search(st, costs, B, epsilon=eps)
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st2 = build_store(layers, cluster, model, imbalance_ratio=rho)
+            plan = search(st2, boundary_costs(layers, cluster), B, epsilon=eps)
+            ts.append(time.perf_counter() - t0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pool, tstar, bs, states, w = sweep_pool(st, costs, B)
+        dt = time.perf_counter() - t0
+        out[name] = {"search_time_s": min(ts), "full_pool_candidates_per_s": len(pool) / dt,
+                     "pool": len(pool), "plan_stages": plan.num_stages,
+                     "T*": plan.predicted_latency}
+    n = 1_000_000
+    f, b, c, S = config_e(n)
+    F, Bt, C, Sd = (torch.from_numpy(x).to(device) for x in (f, b, c, S))
+    for _ in range(2):
+        counts, status = launch_counts_batch(F, Bt, C, kind="adaptive", stage_counts=Sd)
+    torch.cuda.synchronize()
+    dense = torch.zeros((n, 8), dtype=torch.int32, device=device)
+    mask = torch.arange(8, device=device)[None, :] < Sd[:, None].long()
+    dense[mask] = counts
+    simulate_batch(F, Bt, C, dense, 128, stage_counts=Sd)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    counts, status = launch_counts_batch(F, Bt, C, kind="adaptive", stage_counts=Sd)
+    dense[mask] = counts
+    mk, st = simulate_batch(F, Bt, C, dense, 128, stage_counts=Sd)
+    e.record()
+    e.synchronize()
+    dt = s.elapsed_time(e) * 1e-3
+    out["E"] = {"plans": n, "plans_per_s": n / dt, "seconds": dt,
+                "all_ok": bool((st == 0).all().item())}
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

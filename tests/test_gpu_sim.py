@@ -105,7 +105,8 @@ def test_launch_counts_kinds_and_errors():
         adaptive_counts([1.0, 1.0], [1.5])
     with pytest.raises(ScheduleError):
         adaptive_counts([1.0, 1.0], [0.5], t_max=0.5)
-    assert adaptive_counts([1.0, 2.0], [1.5], t_max=3.0).deltas == (3,)
+    assert adaptive_counts([1.0, 2.0], [1.5], t_max=3.0).deltas == (2,)
+    assert adaptive_counts([1.0, 2.0], [1.6], t_max=3.0).deltas == (3,)
     rng = random.Random(7)
     P, S = 200, 5
     t = np.array([[rng.uniform(0.5, 2) for _ in range(S)] for _ in range(P)])

@@ -105,18 +105,17 @@ typedef struct {
 } hapt_model_desc;
 
 /* One CSR entry of the feasible-span index, with everything the DP needs
- * about the transition (o,k)->i besides the layer state. */
+ * about the transition (o,k)->i besides the layer state: 16 bytes, one
+ * 128-bit broadcast load in the DP kernel. */
 typedef struct {
   double tt;        /* t_tab[o,k,i]                                          */
-  int32_t prank;    /* index of tt in the sorted t_max pool                   */
-  int32_t srank;    /* min prank over this entry and the rest of its row     */
-} hapt_span;
-
-typedef struct {
+  int32_t prank;    /* index of tt in the sorted t_max pool (tt <= t_max <=>
+                       prank < #pool values <= t_max); INT32_MAX if tt is
+                       not finite                                            */
   uint16_t i;       /* span end (1-based layer)                              */
   uint16_t kmax;    /* largest integer K with mp + K*ma <= cap (exact fp64),
                        saturated; the _dp.pyx:83 mask becomes kk <= kmax     */
-} hapt_span_ik;
+} hapt_span;
 
 /* Device tables (one instance). Carved out of ONE caller-owned buffer by
  * hapt_tables_init; filled by hapt_tables_build (K1) or, for the drop-in
@@ -137,7 +136,12 @@ typedef struct {
   int32_t *span_off;    /* [n_opts*(L+2)+1]                                  */
   int32_t *span_items;  /* [nnz_cap]                                         */
   hapt_span *spans;     /* [nnz_cap]                                         */
-  hapt_span_ik *span_ik;/* [nnz_cap]                                         */
+  int32_t *span_srank;  /* [nnz_cap] min prank over this entry and the rest of
+                           its row (non-decreasing along the row)            */
+  uint16_t *row_kmin;   /* [n_opts*(L+2)] min kmax over the row: if it is >=
+                           3s the memory mask cannot bind at layer s         */
+  uint16_t *row_pos;    /* [n_opts*(L+2)][L+2] #row entries with span end <= i
+                           (the layer-s scan of a row stops at i = L-s+1)    */
   double *pool;         /* [pool_cap] sorted unique feasible t (t_max candidates) */
   int64_t *counters;    /* [16]: 0 nnz, 1 pool_len, 2..7 StoreStats
                            (candidates, canonical, canonical_feasible, aliased,

@@ -12,7 +12,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libhapt_b200.so")
+LIB_PATH = os.environ.get("HAPT_LIB") or os.path.join(PKG, "libhapt_b200.so")
 
 HAPT_OK = 0
 HAPT_EINVAL = 1
@@ -99,7 +99,9 @@ class Tables(ctypes.Structure):
         ("span_off", c_vp),
         ("span_items", c_vp),
         ("spans", c_vp),
-        ("span_ik", c_vp),
+        ("span_srank", c_vp),
+        ("row_kmin", c_vp),
+        ("row_pos", c_vp),
         ("pool", c_vp),
         ("counters", c_vp),
         ("scratch", c_vp),

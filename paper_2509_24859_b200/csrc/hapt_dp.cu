@@ -32,22 +32,31 @@ namespace hapt {
 namespace {
 
 constexpr int kWarps = 8;  // warps (cells) per block
+#ifndef HAPT_RELAX_MINB
+#define HAPT_RELAX_MINB 4  // resident blocks/SM: 64 registers, no spills (ptxas -v)
+#endif
+#ifndef HAPT_RELAX_UNROLL
+#define HAPT_RELAX_UNROLL 4  // successor loads in flight per warp
+#endif
+constexpr int kU = HAPT_RELAX_UNROLL;
 
 struct Batch {
   // tables
   const hapt_span *spans;
-  const hapt_span_ik *span_ik;
+  const int32_t *span_srank;
+  const uint16_t *row_kmin, *row_pos;
   const int32_t *span_off, *opt_off, *opt_devs, *g_mesh, *g_avail, *g_crow;
   const double *cb;    // cb_same rows then cb_next rows, [2*n_meshes][L+1]
   const double *pool;
   const int64_t *counters;
-  int L, G, s_max, n_cand, n_groups;
+  int L, G, s_max, n_cand, n_groups, rows;
   size_t hg;           // (G+1)*(L+1) successor entries per candidate group
   // per batch
   const double *tmax;  // [n_cand]
   double *tmax_pad;    // [n_groups*32]
   int32_t *tcnt;       // [n_groups*32]  #pool values <= t_max
-  int32_t *gmax;       // [n_groups]     max tcnt in the group
+  uint16_t *cut_sr;    // [n_groups][rows] entries of a row before its suffix-min
+                       // pool rank reaches the group's largest bound
   double *H[2];
   uint16_t *K[2];
   double *ftop;
@@ -56,17 +65,18 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, gmax, H0, H1, K0, K1, total;
+  size_t tmax_pad, tcnt, cut_sr, H0, H1, K0, K1, total;
 };
 
 WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   WsLayout w{};
   const size_t ng = (size_t)(n_cand + 31) / 32, np = ng * 32;
   const size_t hg = (size_t)(t->G + 1) * (t->L + 1);
+  const size_t rows = (size_t)t->n_opts * (t->L + 2);
   size_t cur = 0;
   w.tmax_pad = cur; cur += align_up(np * 8);
   w.tcnt = cur; cur += align_up(np * 4);
-  w.gmax = cur; cur += align_up(ng * 4);
+  w.cut_sr = cur; cur += align_up(ng * rows * 2);
   w.H0 = cur; cur += align_up(ng * hg * 32 * 8);
   w.H1 = cur; cur += align_up(ng * hg * 32 * 8);
   w.K0 = cur; cur += align_up(ng * hg * 32 * 2);
@@ -84,24 +94,24 @@ __device__ __forceinline__ int upper_bound(const double *a, int n, double v) {
   return lo;
 }
 
-// Candidate padding, pool ranks, and the layer-0 successor table:
-// F[0, L+1, 0] = 0 (_dp.pyx:41) is the only finite base state.
+// Per group: candidate padding, pool ranks, the per-row suffix-rank cut, and
+// the layer-0 successor table: F[0, L+1, 0] = 0 (_dp.pyx:41) is the only
+// finite base state.
 __global__ void dp_prep(Batch b) {
+  __shared__ int s_gmax;
   const int lane = threadIdx.x & 31;
   const int group = blockIdx.x;
   const int cand = group * 32 + lane;
   const int src = cand < b.n_cand ? cand : b.n_cand - 1;
   const double tm = b.tmax[src];
-  const int plen = (int)b.counters[1];
-  const int cnt = upper_bound(b.pool, plen, tm);
   if (threadIdx.x < 32) {
+    const int cnt = upper_bound(b.pool, (int)b.counters[1], tm);
     b.tmax_pad[cand] = tm;
     b.tcnt[cand] = cnt;
     int m = cnt;
     for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (lane == 0) b.gmax[group] = m;
+    if (lane == 0) s_gmax = m;
   }
-  // layer-0 table for this group: everything +inf except (g2 = 0, i = L)
   double *H = b.H[0] + (size_t)group * b.hg * 32;
   uint16_t *K = b.K[0] + (size_t)group * b.hg * 32;
   for (size_t x = threadIdx.x; x < b.hg * 32; x += blockDim.x) {
@@ -109,6 +119,18 @@ __global__ void dp_prep(Batch b) {
     K[x] = 0;
   }
   __syncthreads();
+  // suffix-min ranks are non-decreasing along a row: first entry no lane of
+  // this group can accept (prank >= srank >= max tcnt) ends the row's scan
+  const int gm = s_gmax;
+  for (int row = threadIdx.x; row < b.rows; row += blockDim.x) {
+    const int beg = b.span_off[row], end = b.span_off[row + 1];
+    int lo = beg, hi = end;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (b.span_srank[mid] < gm) lo = mid + 1; else hi = mid;
+    }
+    b.cut_sr[(size_t)group * b.rows + row] = (uint16_t)(lo - beg);
+  }
   if (threadIdx.x < 32) {
     const int row = b.g_crow[0];
     const double c = b.cb[(size_t)row * (b.L + 1) + b.L];
@@ -121,61 +143,140 @@ __global__ void dp_prep(Batch b) {
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) dp_relax(Batch b, int s, int group0) {
+// The transitions of one cell, flattened over its admissible (option, split)
+// entries in the reference's order (o ascending, i ascending, _dp.pyx:58,67)
+// and staged in shared memory as {tt, prank, key = o<<20 | g2*(L+1)+i}.
+// Each lane (= candidate) keeps the first strict minimum, exactly the
+// reference's `cand < best` update.  Successor values are requested four at
+// a time so their latencies overlap.
+template <bool WITH_KK>
+__device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
+                                              const uint16_t *__restrict__ skm, int n, int cnt,
+                                              const double *__restrict__ Hg,
+                                              const uint16_t *__restrict__ Kg, double &bv,
+                                              int &bkey, int &bkk) {
+  for (int u = 0; u < n; u += kU) {
+    int4 ex[kU];
+    double h[kU];
+    int kk[kU], km[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      h[q] = kInf;
+      kk[q] = 0;
+      km[q] = 0;
+      ex[q] = make_int4(0, 0, 0x7fffffff, 0);
+      if (u + q < n) {
+        ex[q] = st[u + q];
+        const int hoff = ex[q].w & 0xfffff;
+        h[q] = __ldg(Hg + (size_t)hoff * 32);
+        if (WITH_KK) {
+          kk[q] = __ldg(Kg + (size_t)hoff * 32);
+          km[q] = skm[u + q];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const double c = __dadd_rn(__hiloint2double(ex[q].y, ex[q].x), h[q]);  // tt + (2c+F)
+      if (u + q < n && ex[q].z < cnt && (!WITH_KK || kk[q] <= km[q]) && c < bv) {
+        bv = c;
+        bkey = ex[q].w;
+        bkk = WITH_KK ? kk[q] : -1;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b, int s, int group0) {
   __shared__ int fin_cnt[kWarps][32];
+  __shared__ int4 stage_e[kWarps][32];
+  __shared__ uint16_t stage_k[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int group = group0 + blockIdx.y;
   const int L = b.L, G = b.G;
   const int nk = L - s + 1, ng = G - s + 1;
-  const long cell = (long)blockIdx.x * kWarps + warp;
-  const bool active = cell < (long)nk * ng;
+  const int cell = blockIdx.x * kWarps + warp;
+  const bool active = cell < nk * ng;
   const int cand = group * 32 + lane;
   int fin = 0;
   if (active) {
-    const int k = 1 + (int)(cell % nk);
-    const int g = s + (int)(cell / nk);
+    const int k = 1 + cell % nk;
+    const int g = s + cell / nk;
     const double tm = b.tmax_pad[cand];
     const int cnt = b.tcnt[cand];
-    const int maxcnt = b.gmax[group];
     const int imax = L - s + 1;
-    const int r = b.g_mesh[g], avail = b.g_avail[g];
+    const int r = b.g_mesh[g];
+    const int o0 = b.opt_off[r], nopt = b.opt_off[r + 1] - o0;
     const size_t gbase = (size_t)group * b.hg;
-    const double *Hin = b.H[(s - 1) & 1];
-    const uint16_t *Kin = b.K[(s - 1) & 1];
-    double best = kInf;
-    int bo = -1, bi = -1, bkk = 0;
-    const int o_end = b.opt_off[r + 1];
-    for (int o = b.opt_off[r]; o < o_end; ++o) {
-      const int devs = b.opt_devs[o];
-      if (devs > avail) continue;
-      const int g2 = g - devs;
-      if (g2 < s - 1) continue;
-      const int row = o * (L + 2) + k;
-      const int beg = b.span_off[row], end = b.span_off[row + 1];
-      const size_t base = (gbase + (size_t)g2 * (L + 1)) * 32 + lane;
-      const double *Hr = Hin + base;
-      const uint16_t *Kr = Kin + base;
-      for (int idx = beg; idx < end; ++idx) {
-        const hapt_span e = b.spans[idx];
-        const hapt_span_ik ik = b.span_ik[idx];
-        if (ik.i > imax || e.srank >= maxcnt) break;
-        const double h = Hr[(size_t)ik.i * 32];
-        const int kk = Kr[(size_t)ik.i * 32];
-        const double c = __dadd_rn(e.tt, h);  // tt + (2c + F)  (_dp.pyx:85)
-        if (e.prank < cnt && kk <= ik.kmax && c < best) {
-          best = c;
-          bo = o;
-          bi = ik.i;
-          bkk = kk;
+    const double *Hg = b.H[(s - 1) & 1] + gbase * 32 + lane;
+    const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * 32 + lane;
+    double bv = kInf;
+    int bkey = -1, bkk = 0;
+    // options of mesh r, 32 at a time (a mesh rarely has more than 32 submesh
+    // shapes); rows are visited in ascending option order
+    for (int c0 = 0; c0 < nopt; c0 += 32) {
+      const int nch = min(32, nopt - c0);
+      // lane j: admissible entries of option o0+c0+j's row (k) at this layer
+      int len = 0, beg = 0, hbase = 0;
+      bool needkk = false;
+      if (lane < nch) {
+        const int o = o0 + c0 + lane;
+        const int devs = b.opt_devs[o], g2 = g - devs;
+        if (devs <= b.g_avail[g] && g2 >= s - 1) {
+          const int row = o * (L + 2) + k;
+          beg = b.span_off[row];
+          // entries with i <= L-s+1 (later successors are provably infinite)
+          // and before the group's suffix-rank cut
+          len = min((int)b.row_pos[(size_t)row * (L + 2) + imax],
+                    (int)b.cut_sr[(size_t)group * b.rows + row]);
+          hbase = g2 * (L + 1);
+          // KK <= 3s at layer s: ceil(2c/t_max) <= 2 and N grows by <= 3 per
+          // stage, so a row whose thresholds are all >= 3s cannot fail the
+          // memory mask (_dp.pyx:83)
+          needkk = len > 0 && (int)b.row_kmin[row] < 3 * s;
         }
       }
+      int incl = len;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      const int T = __shfl_sync(0xffffffffu, incl, 31);
+      const int start = incl - len;
+      const bool anykk = __any_sync(0xffffffffu, needkk);
+      for (int r0 = 0; r0 < T; r0 += 32) {
+        const int t = r0 + lane;
+        int j = 0;  // owner row: number of rows whose entries end at or before t
+        for (int q = 0; q < nch; ++q) j += (__shfl_sync(0xffffffffu, incl, q) <= t);
+        const int jj = min(j, 31);
+        const int ob = __shfl_sync(0xffffffffu, beg, jj);
+        const int os = __shfl_sync(0xffffffffu, start, jj);
+        const int oh = __shfl_sync(0xffffffffu, hbase, jj);
+        if (t < T) {
+          const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
+          stage_e[warp][lane] =
+              make_int4(x.x, x.y, x.z, ((o0 + c0 + j) << 20) | (oh + (x.w & 0xffff)));
+          stage_k[warp][lane] = (uint16_t)((unsigned)x.w >> 16);
+        }
+        __syncwarp();
+        const int n = min(32, T - r0);
+        if (anykk)
+          relax_entries<true>(stage_e[warp], stage_k[warp], n, cnt, Hg, Kg, bv, bkey, bkk);
+        else
+          relax_entries<false>(stage_e[warp], stage_k[warp], n, cnt, Hg, Kg, bv, bkey, bkk);
+        __syncwarp();
+      }
     }
-    fin = bo >= 0;
+    fin = bkey >= 0;
+    const int bo = bkey >> 20, boff = bkey & 0xfffff;
+    const int bi = boff % (L + 1);
+    if (fin && bkk < 0) bkk = __ldg(Kg + (size_t)boff * 32);
     if (cand < b.n_cand) {
-      if (k == 1 && g == G) b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
+      if (k == 1 && g == G) b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv;
       if (fin && b.full.bp_o) {
         const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
-        if (b.full.F) b.full.F[e] = best;
+        if (b.full.F) b.full.F[e] = bv;
         if (b.full.N) b.full.N[e] = (double)bkk;
         b.full.bp_i[e] = bi;
         b.full.bp_o[e] = bo;
@@ -190,7 +291,7 @@ __global__ void __launch_bounds__(kWarps * 32) dp_relax(Batch b, int s, int grou
         const double c = b.cb[(size_t)crow * (L + 1) + (k - 1)];
         if (c <= tm) {
           const double c2 = __dmul_rn(2.0, c);
-          hn = __dadd_rn(c2, best);
+          hn = __dadd_rn(c2, bv);
           kn = (int)ceil(__ddiv_rn(c2, tm)) + 1 + bkk;
         }
       }
@@ -347,7 +448,10 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   char *wb = (char *)work;
   Batch b{};
   b.spans = t->spans;
-  b.span_ik = t->span_ik;
+  b.span_srank = t->span_srank;
+  b.row_kmin = t->row_kmin;
+  b.row_pos = t->row_pos;
+  b.rows = t->n_opts * (t->L + 2);
   b.span_off = t->span_off;
   b.opt_off = t->opt_off;
   b.opt_devs = t->opt_devs;
@@ -366,7 +470,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.tmax = tmax;
   b.tmax_pad = (double *)(wb + w.tmax_pad);
   b.tcnt = (int32_t *)(wb + w.tcnt);
-  b.gmax = (int32_t *)(wb + w.gmax);
+  b.cut_sr = (uint16_t *)(wb + w.cut_sr);
   b.H[0] = (double *)(wb + w.H0);
   b.H[1] = (double *)(wb + w.H1);
   b.K[0] = (uint16_t *)(wb + w.K0);

@@ -65,17 +65,19 @@ Layout layout(int L, int G, int n_opts, int n_meshes) {
   sz[n++] = (y.rows + 1) * 4;                             // 17 span_off
   sz[n++] = y.nnz_cap * 4;                                // 18 span_items
   sz[n++] = y.nnz_cap * sizeof(hapt_span);                // 19 spans
-  sz[n++] = y.nnz_cap * sizeof(hapt_span_ik);             // 20 span_ik
+  sz[n++] = y.nnz_cap * 4;                                // 20 span_srank
   sz[n++] = y.pool_cap * 8;                               // 21 pool
   sz[n++] = 16 * 8;                                       // 22 counters
+  sz[n++] = y.rows * 2;                                   // 23 row_kmin
   // scratch
-  sz[n++] = (size_t)3 * (L + 1) * 8;                      // 23 prefix sums
-  sz[n++] = (size_t)(L + 2) * (L + 2) * 4;                // 24 lcp
-  sz[n++] = (y.rows + 1) * 4;                             // 25 row counts
-  sz[n++] = y.nnz_cap * 8;                                // 26 keys a
-  sz[n++] = y.nnz_cap * 8;                                // 27 keys b
-  sz[n++] = (y.pool_cap + 1) * 8;                         // 28 rank histogram / scan
-  sz[n++] = kCubTempBase + y.nnz_cap * 16;                // 29 cub temp
+  sz[n++] = (size_t)3 * (L + 1) * 8;                      // 24 prefix sums
+  sz[n++] = (size_t)(L + 2) * (L + 2) * 4;                // 25 lcp
+  sz[n++] = (y.rows + 1) * 4;                             // 26 row counts
+  sz[n++] = y.nnz_cap * 8;                                // 27 keys a
+  sz[n++] = y.nnz_cap * 8;                                // 28 keys b
+  sz[n++] = (y.pool_cap + 1) * 8;                         // 29 rank histogram / scan
+  sz[n++] = kCubTempBase + y.nnz_cap * 16;                // 30 cub temp
+  sz[n++] = y.rows * (size_t)(L + 2) * 2;                 // 31 row_pos (table, after scratch)
   size_t cur = 0;
   for (int i = 0; i < n; ++i) {
     y.off[i] = cur;
@@ -99,13 +101,13 @@ Scratch scratch_of(const hapt_tables *t) {
   Layout y = layout(t->L, t->G, t->n_opts, t->n_meshes);
   char *base = (char *)t->t_tab;  // buffer start
   Scratch s;
-  s.prefix = (double *)(base + y.off[23]);
-  s.lcp = (int32_t *)(base + y.off[24]);
-  s.row_cnt = (int32_t *)(base + y.off[25]);
-  s.keys_a = (unsigned long long *)(base + y.off[26]);
-  s.keys_b = (unsigned long long *)(base + y.off[27]);
-  s.hist = (long long *)(base + y.off[28]);
-  s.cub_temp = base + y.off[29];
+  s.prefix = (double *)(base + y.off[24]);
+  s.lcp = (int32_t *)(base + y.off[25]);
+  s.row_cnt = (int32_t *)(base + y.off[26]);
+  s.keys_a = (unsigned long long *)(base + y.off[27]);
+  s.keys_b = (unsigned long long *)(base + y.off[28]);
+  s.hist = (long long *)(base + y.off[29]);
+  s.cub_temp = base + y.off[30];
   s.cub_bytes = kCubTempBase + y.nnz_cap * 16;
   return s;
 }
@@ -337,20 +339,21 @@ __global__ void k_span_meta(hapt_tables t, unsigned long long *keys) {
   const int o = (int)(r / S);
   const double cap = t.opt_cap[o];
   const double *trow = t.t_tab + r * S, *mrow = t.mp_tab + r * S, *arow = t.ma_tab + r * S;
+  int kmin = kKSat;
   for (int idx = t.span_off[r]; idx < t.span_off[r + 1]; ++idx) {
     const int p = t.span_items[idx];
     const double tt = trow[p];
     hapt_span sp;
     sp.tt = tt;
     sp.prank = 0;
-    sp.srank = 0;
+    sp.i = (uint16_t)p;
+    const int km = mem_kmax(mrow[p], arow[p], cap);
+    sp.kmax = (uint16_t)km;
+    kmin = min(kmin, km);
     t.spans[idx] = sp;
-    hapt_span_ik ik;
-    ik.i = (uint16_t)p;
-    ik.kmax = (uint16_t)mem_kmax(mrow[p], arow[p], cap);
-    t.span_ik[idx] = ik;
     keys[idx] = isfinite(tt) ? fkey(tt) : kPadKey;
   }
+  t.row_kmin[r] = (uint16_t)kmin;
 }
 
 __global__ void k_pool_decode(hapt_tables t, const unsigned long long *uniq,
@@ -382,13 +385,23 @@ __global__ void k_prank(hapt_tables t) {
   t.spans[idx].prank = isfinite(tt) ? lower_bound(t.pool, (int)t.counters[1], tt) : 0x7fffffff;
 }
 
+// Row suffix-min pool ranks and the per-row position table row_pos[row][i]
+// = #entries with span end <= i (entries are in ascending span end).
 __global__ void k_srank(hapt_tables t) {
   const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= (long)t.n_opts * (t.L + 2)) return;
+  const int S = t.L + 2;
+  if (r >= (long)t.n_opts * S) return;
   int m = 0x7fffffff;
-  for (int idx = t.span_off[r + 1] - 1; idx >= t.span_off[r]; --idx) {
+  const int beg = t.span_off[r], end = t.span_off[r + 1];
+  for (int idx = end - 1; idx >= beg; --idx) {
     m = min(m, t.spans[idx].prank);
-    t.spans[idx].srank = m;
+    t.span_srank[idx] = m;
+  }
+  uint16_t *pos = t.row_pos + r * S;
+  int idx = beg;
+  for (int i = 0; i < S; ++i) {
+    while (idx < end && t.spans[idx].i <= i) ++idx;
+    pos[i] = (uint16_t)(idx - beg);
   }
 }
 
@@ -483,6 +496,11 @@ extern "C" int hapt_tables_init(hapt_tables *t, void *buf, size_t buf_bytes, int
   t->n_opts = n_opts;
   t->n_meshes = n_meshes;
   t->s_max = L < G ? L : G;
+  if ((size_t)(G + 1) * (L + 1) >= (1u << 20) || n_opts >= 2048) {
+    set_error("hapt_tables_init: (G+1)(L+1)=%zu or n_opts=%d exceeds the packed transition key",
+              (size_t)(G + 1) * (L + 1), n_opts);
+    return HAPT_EINVAL;
+  }
   if (3 * t->s_max + 3 >= kKSat) {
     set_error("hapt_tables_init: s_max=%d too large for 16-bit launch bounds", t->s_max);
     return HAPT_EINVAL;
@@ -510,11 +528,13 @@ extern "C" int hapt_tables_init(hapt_tables *t, void *buf, size_t buf_bytes, int
   t->span_off = (int32_t *)(b + y.off[17]);
   t->span_items = (int32_t *)(b + y.off[18]);
   t->spans = (hapt_span *)(b + y.off[19]);
-  t->span_ik = (hapt_span_ik *)(b + y.off[20]);
+  t->span_srank = (int32_t *)(b + y.off[20]);
   t->pool = (double *)(b + y.off[21]);
   t->counters = (int64_t *)(b + y.off[22]);
-  t->scratch = b + y.off[23];
-  t->scratch_bytes = y.total - y.off[23];
+  t->row_kmin = (uint16_t *)(b + y.off[23]);
+  t->row_pos = (uint16_t *)(b + y.off[31]);
+  t->scratch = b + y.off[24];
+  t->scratch_bytes = y.off[31] - y.off[24];
   return HAPT_OK;
 }
 

@@ -14,6 +14,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="D1")
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--time", type=int, default=0, help="timed sweeps after warm-up")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -29,6 +30,18 @@ def main():
     for _ in range(args.repeat):
         ftop, states = tables.sweeper.sweep_device(tmax)
     torch.cuda.synchronize()
+    if args.time:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.time):
+            ftop, states = tables.sweeper.sweep_device(tmax)
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e) / args.time
+        trans = tables.transitions_per_sweep()
+        print(f"{args.config} lib={os.environ.get('HAPT_LIB', 'default')} pool={len(tmax)} "
+              f"sweep={ms:.3f} ms  cand/s={len(tmax) / ms * 1e3:.0f}  "
+              f"transitions/s={trans * len(tmax) / ms * 1e3:.3e}")
     print("ok", int(states.sum()))
 
 

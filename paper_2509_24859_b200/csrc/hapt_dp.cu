@@ -145,43 +145,36 @@ __global__ void dp_prep(Batch b) {
 
 // The transitions of one cell, flattened over its admissible (option, split)
 // entries in the reference's order (o ascending, i ascending, _dp.pyx:58,67)
-// and staged in shared memory as {tt, prank, key = o<<20 | g2*(L+1)+i}.
-// Each lane (= candidate) keeps the first strict minimum, exactly the
-// reference's `cand < best` update.  Successor values are requested four at
-// a time so their latencies overlap.
+// and staged in shared memory as
+//     {tt (2 words), w2 = prank*2048 + o, w3 = byte offset of the successor}
+// so `tt <= t_max` is `w2 < cnt*2048` (o < 2048) and the option of the
+// winner rides along for free.  The stage is padded to a multiple of kU with
+// inert entries (w2 = ~0 never passes), so the loop has no guards.  Each lane
+// (= candidate) keeps the first strict minimum, exactly the reference's
+// `cand < best` update; kU successor loads are in flight per warp.
 template <bool WITH_KK>
 __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
-                                              const uint16_t *__restrict__ skm, int n, int cnt,
-                                              const double *__restrict__ Hg,
-                                              const uint16_t *__restrict__ Kg, double &bv,
-                                              int &bkey, int &bkk) {
+                                              const uint16_t *__restrict__ skm, int n,
+                                              unsigned cnt2, const char *__restrict__ Hb,
+                                              const char *__restrict__ Kb, double &bv,
+                                              unsigned &bw2, unsigned &bw3) {
   for (int u = 0; u < n; u += kU) {
     int4 ex[kU];
     double h[kU];
-    int kk[kU], km[kU];
+    int kk[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      h[q] = kInf;
-      kk[q] = 0;
-      km[q] = 0;
-      ex[q] = make_int4(0, 0, 0x7fffffff, 0);
-      if (u + q < n) {
-        ex[q] = st[u + q];
-        const int hoff = ex[q].w & 0xfffff;
-        h[q] = __ldg(Hg + (size_t)hoff * 32);
-        if (WITH_KK) {
-          kk[q] = __ldg(Kg + (size_t)hoff * 32);
-          km[q] = skm[u + q];
-        }
-      }
+      ex[q] = st[u + q];
+      h[q] = __ldg(reinterpret_cast<const double *>(Hb + (unsigned)ex[q].w));
+      if (WITH_KK) kk[q] = __ldg(reinterpret_cast<const uint16_t *>(Kb + ((unsigned)ex[q].w >> 2)));
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
       const double c = __dadd_rn(__hiloint2double(ex[q].y, ex[q].x), h[q]);  // tt + (2c+F)
-      if (u + q < n && ex[q].z < cnt && (!WITH_KK || kk[q] <= km[q]) && c < bv) {
+      if ((unsigned)ex[q].z < cnt2 && (!WITH_KK || kk[q] <= (int)skm[u + q]) && c < bv) {
         bv = c;
-        bkey = ex[q].w;
-        bkk = WITH_KK ? kk[q] : -1;
+        bw2 = (unsigned)ex[q].z;
+        bw3 = (unsigned)ex[q].w;
       }
     }
   }
@@ -210,8 +203,11 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
     const size_t gbase = (size_t)group * b.hg;
     const double *Hg = b.H[(s - 1) & 1] + gbase * 32 + lane;
     const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * 32 + lane;
+    const char *Hb = reinterpret_cast<const char *>(Hg);
+    const char *Kb = reinterpret_cast<const char *>(Kg);
+    const unsigned cnt2 = (unsigned)cnt << 11;
     double bv = kInf;
-    int bkey = -1, bkk = 0;
+    unsigned bw2 = ~0u, bw3 = 0;
     // options of mesh r, 32 at a time (a mesh rarely has more than 32 submesh
     // shapes); rows are visited in ascending option order
     for (int c0 = 0; c0 < nopt; c0 += 32) {
@@ -253,25 +249,30 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
         const int ob = __shfl_sync(0xffffffffu, beg, jj);
         const int os = __shfl_sync(0xffffffffu, start, jj);
         const int oh = __shfl_sync(0xffffffffu, hbase, jj);
+        int4 se = make_int4(0, 0, -1, 0);  // inert padding entry
+        uint16_t sk = 0;
         if (t < T) {
           const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
-          stage_e[warp][lane] =
-              make_int4(x.x, x.y, x.z, ((o0 + c0 + j) << 20) | (oh + (x.w & 0xffff)));
-          stage_k[warp][lane] = (uint16_t)((unsigned)x.w >> 16);
+          const unsigned w2 = x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
+          se = make_int4(x.x, x.y, (int)w2, (oh + (x.w & 0xffff)) * 256);
+          sk = (uint16_t)((unsigned)x.w >> 16);
         }
+        stage_e[warp][lane] = se;
+        stage_k[warp][lane] = sk;
         __syncwarp();
         const int n = min(32, T - r0);
         if (anykk)
-          relax_entries<true>(stage_e[warp], stage_k[warp], n, cnt, Hg, Kg, bv, bkey, bkk);
+          relax_entries<true>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
         else
-          relax_entries<false>(stage_e[warp], stage_k[warp], n, cnt, Hg, Kg, bv, bkey, bkk);
+          relax_entries<false>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
         __syncwarp();
       }
     }
-    fin = bkey >= 0;
-    const int bo = bkey >> 20, boff = bkey & 0xfffff;
+    fin = bw2 != ~0u;
+    const int bo = (int)(bw2 & 2047u), boff = (int)(bw3 >> 8);
     const int bi = boff % (L + 1);
-    if (fin && bkk < 0) bkk = __ldg(Kg + (size_t)boff * 32);
+    // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
+    const int bkk = fin ? (int)__ldg(Kg + (size_t)boff * 32) : 0;
     if (cand < b.n_cand) {
       if (k == 1 && g == G) b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv;
       if (fin && b.full.bp_o) {

@@ -496,7 +496,8 @@ extern "C" int hapt_tables_init(hapt_tables *t, void *buf, size_t buf_bytes, int
   t->n_opts = n_opts;
   t->n_meshes = n_meshes;
   t->s_max = L < G ? L : G;
-  if ((size_t)(G + 1) * (L + 1) >= (1u << 20) || n_opts >= 2048) {
+  if ((size_t)(G + 1) * (L + 1) >= (1u << 20) || n_opts >= 2048 ||
+      (size_t)n_opts * L * (L + 1) / 2 >= (1u << 21)) {
     set_error("hapt_tables_init: (G+1)(L+1)=%zu or n_opts=%d exceeds the packed transition key",
               (size_t)(G + 1) * (L + 1), n_opts);
     return HAPT_EINVAL;

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", default="D1")
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--time", type=int, default=0, help="timed sweeps after warm-up")
+    ap.add_argument("--ws-mb", type=int, default=0, help="cap the DP workspace (MB) -> chunking")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -26,6 +27,8 @@ def main():
     layers, cluster, model, rho, B, eps = instance(args.config)
     store = build_store(layers, cluster, model, imbalance_ratio=rho)
     tables = DpTables(store, boundary_costs(layers, cluster))
+    if args.ws_mb:
+        tables.sweeper.max_ws_bytes = args.ws_mb << 20
     tmax = torch.from_numpy(np.asarray(store.feasible_t_values())).cuda()
     for _ in range(args.repeat):
         ftop, states = tables.sweeper.sweep_device(tmax)

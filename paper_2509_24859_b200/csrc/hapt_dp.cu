@@ -26,6 +26,8 @@
 //    rank lets a warp stop a row once no lane can accept a later span;
 //  * provably infinite cells/transitions (g < s, L-k+1 < s, i > L-s+1,
 //    g2 < s-1) are never visited.
+#include <stdlib.h>
+
 #include "hapt_common.cuh"
 
 namespace hapt {
@@ -33,12 +35,29 @@ namespace {
 
 constexpr int kWarps = 8;  // warps (cells) per block
 #ifndef HAPT_RELAX_MINB
-#define HAPT_RELAX_MINB 4  // resident blocks/SM: 64 registers, no spills (ptxas -v)
+#define HAPT_RELAX_MINB 4  // resident blocks/SM (64 registers, no spills: ptxas -v)
 #endif
-#ifndef HAPT_RELAX_UNROLL
-#define HAPT_RELAX_UNROLL 4  // successor loads in flight per warp
-#endif
-constexpr int kU = HAPT_RELAX_UNROLL;
+
+// Candidates per lane.  A group of 32*CPL candidates shares one warp per DP
+// cell: the staged CSR entry, the address arithmetic and one vector load of
+// the successor values serve CPL candidates at once.
+// Two per lane once the first layer alone has ~3.5 full GPU loads of warps
+// (148 SMs x 32 resident warps); below that, one per lane keeps more warps
+// in flight (measured: D1/C faster with 2, B faster with 1).  HAPT_CPL=1|2|4
+// overrides for experiments.
+int cpl_for(const hapt_tables *t, int n_cand) {
+  if (const char *e = getenv("HAPT_CPL")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4) return v;
+  }
+  const long warps2 = (long)t->L * t->G * ((n_cand + 63) / 64);
+  return warps2 >= 16384 ? 2 : 1;
+}
+
+template <int CPL>
+struct Unroll {
+  static constexpr int value = CPL >= 4 ? 2 : 4;  // successor loads in flight per warp
+};
 
 struct Batch {
   // tables
@@ -49,15 +68,15 @@ struct Batch {
   const double *cb;    // cb_same rows then cb_next rows, [2*n_meshes][L+1]
   const double *pool;
   const int64_t *counters;
-  int L, G, s_max, n_cand, n_groups, rows;
+  int L, G, s_max, n_cand, n_groups, rows, cpl, cw;
   size_t hg;           // (G+1)*(L+1) successor entries per candidate group
   // per batch
   const double *tmax;  // [n_cand]
-  double *tmax_pad;    // [n_groups*32]
-  int32_t *tcnt;       // [n_groups*32]  #pool values <= t_max
+  double *tmax_pad;    // [n_groups*cw]
+  int32_t *tcnt;       // [n_groups*cw]  #pool values <= t_max
   uint16_t *cut_sr;    // [n_groups][rows] entries of a row before its suffix-min
                        // pool rank reaches the group's largest bound
-  double *H[2];
+  double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
   double *ftop;
   unsigned long long *states;
@@ -70,17 +89,18 @@ struct WsLayout {
 
 WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   WsLayout w{};
-  const size_t ng = (size_t)(n_cand + 31) / 32, np = ng * 32;
+  const size_t cw = 32 * (size_t)cpl_for(t, n_cand);
+  const size_t ng = (n_cand + cw - 1) / cw, np = ng * cw;
   const size_t hg = (size_t)(t->G + 1) * (t->L + 1);
   const size_t rows = (size_t)t->n_opts * (t->L + 2);
   size_t cur = 0;
   w.tmax_pad = cur; cur += align_up(np * 8);
   w.tcnt = cur; cur += align_up(np * 4);
   w.cut_sr = cur; cur += align_up(ng * rows * 2);
-  w.H0 = cur; cur += align_up(ng * hg * 32 * 8);
-  w.H1 = cur; cur += align_up(ng * hg * 32 * 8);
-  w.K0 = cur; cur += align_up(ng * hg * 32 * 2);
-  w.K1 = cur; cur += align_up(ng * hg * 32 * 2);
+  w.H0 = cur; cur += align_up(ng * hg * cw * 8);
+  w.H1 = cur; cur += align_up(ng * hg * cw * 8);
+  w.K0 = cur; cur += align_up(ng * hg * cw * 2);
+  w.K1 = cur; cur += align_up(ng * hg * cw * 2);
   w.total = cur;
   return w;
 }
@@ -99,28 +119,27 @@ __device__ __forceinline__ int upper_bound(const double *a, int n, double v) {
 // finite base state.
 __global__ void dp_prep(Batch b) {
   __shared__ int s_gmax;
-  const int lane = threadIdx.x & 31;
   const int group = blockIdx.x;
-  const int cand = group * 32 + lane;
-  const int src = cand < b.n_cand ? cand : b.n_cand - 1;
-  const double tm = b.tmax[src];
-  if (threadIdx.x < 32) {
-    const int cnt = upper_bound(b.pool, (int)b.counters[1], tm);
-    b.tmax_pad[cand] = tm;
-    b.tcnt[cand] = cnt;
-    int m = cnt;
-    for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (lane == 0) s_gmax = m;
-  }
-  double *H = b.H[0] + (size_t)group * b.hg * 32;
-  uint16_t *K = b.K[0] + (size_t)group * b.hg * 32;
-  for (size_t x = threadIdx.x; x < b.hg * 32; x += blockDim.x) {
+  const int cw = b.cw;
+  if (threadIdx.x == 0) s_gmax = 0;
+  __syncthreads();
+  double *H = b.H[0] + (size_t)group * b.hg * cw;
+  uint16_t *K = b.K[0] + (size_t)group * b.hg * cw;
+  for (size_t x = threadIdx.x; x < b.hg * cw; x += blockDim.x) {
     H[x] = kInf;
     K[x] = 0;
   }
+  if (threadIdx.x < cw) {
+    const int cand = group * cw + threadIdx.x;
+    const double tm = b.tmax[cand < b.n_cand ? cand : b.n_cand - 1];
+    const int cnt = upper_bound(b.pool, (int)b.counters[1], tm);
+    b.tmax_pad[cand] = tm;
+    b.tcnt[cand] = cnt;
+    atomicMax(&s_gmax, cnt);
+  }
   __syncthreads();
-  // suffix-min ranks are non-decreasing along a row: first entry no lane of
-  // this group can accept (prank >= srank >= max tcnt) ends the row's scan
+  // suffix-min ranks are non-decreasing along a row: first entry no candidate
+  // of this group can accept (prank >= srank >= max tcnt) ends the row's scan
   const int gm = s_gmax;
   for (int row = threadIdx.x; row < b.rows; row += blockDim.x) {
     const int beg = b.span_off[row], end = b.span_off[row + 1];
@@ -131,10 +150,11 @@ __global__ void dp_prep(Batch b) {
     }
     b.cut_sr[(size_t)group * b.rows + row] = (uint16_t)(lo - beg);
   }
-  if (threadIdx.x < 32) {
+  if (threadIdx.x < cw) {
+    const double tm = b.tmax_pad[group * cw + threadIdx.x];
     const int row = b.g_crow[0];
     const double c = b.cb[(size_t)row * (b.L + 1) + b.L];
-    const size_t e = (size_t)b.L * 32 + lane;  // g2 = 0, i = L
+    const size_t e = (size_t)b.L * cw + threadIdx.x;  // g2 = 0, i = L
     if (c <= tm) {
       const double c2 = __dmul_rn(2.0, c);
       H[e] = __dadd_rn(c2, 0.0);
@@ -143,45 +163,85 @@ __global__ void dp_prep(Batch b) {
   }
 }
 
+template <int CPL>
+__device__ __forceinline__ void load_h(const char *p, double (&h)[CPL]) {
+  if constexpr (CPL == 1) {
+    h[0] = __ldg(reinterpret_cast<const double *>(p));
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; c += 2) {
+      const double2 v = __ldg(reinterpret_cast<const double2 *>(p) + c / 2);
+      h[c] = v.x;
+      h[c + 1] = v.y;
+    }
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void load_k(const char *p, int (&k)[CPL]) {
+  if constexpr (CPL == 1) {
+    k[0] = __ldg(reinterpret_cast<const uint16_t *>(p));
+  } else if constexpr (CPL == 2) {
+    const unsigned v = __ldg(reinterpret_cast<const unsigned *>(p));
+    k[0] = v & 0xffff;
+    k[1] = v >> 16;
+  } else {
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+    k[0] = v.x & 0xffff;
+    k[1] = v.x >> 16;
+    k[2] = v.y & 0xffff;
+    k[3] = v.y >> 16;
+  }
+}
+
 // The transitions of one cell, flattened over its admissible (option, split)
 // entries in the reference's order (o ascending, i ascending, _dp.pyx:58,67)
 // and staged in shared memory as
 //     {tt (2 words), w2 = prank*2048 + o, w3 = byte offset of the successor}
 // so `tt <= t_max` is `w2 < cnt*2048` (o < 2048) and the option of the
-// winner rides along for free.  The stage is padded to a multiple of kU with
-// inert entries (w2 = ~0 never passes), so the loop has no guards.  Each lane
-// (= candidate) keeps the first strict minimum, exactly the reference's
-// `cand < best` update; kU successor loads are in flight per warp.
-template <bool WITH_KK>
+// winner rides along for free.  The stage is padded to a multiple of the
+// unroll with inert entries (w2 = ~0 never passes), so the loop has no
+// guards.  Every candidate keeps the first strict minimum, exactly the
+// reference's `cand < best` update.
+template <bool WITH_KK, int CPL>
 __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
                                               const uint16_t *__restrict__ skm, int n,
-                                              unsigned cnt2, const char *__restrict__ Hb,
-                                              const char *__restrict__ Kb, double &bv,
-                                              unsigned &bw2, unsigned &bw3) {
-  for (int u = 0; u < n; u += kU) {
-    int4 ex[kU];
-    double h[kU];
-    int kk[kU];
+                                              const unsigned (&cnt2)[CPL],
+                                              const char *__restrict__ Hb,
+                                              const char *__restrict__ Kb, double (&bv)[CPL],
+                                              unsigned (&bw2)[CPL], unsigned (&bw3)[CPL]) {
+  constexpr int U = Unroll<CPL>::value;
+  for (int u = 0; u < n; u += U) {
+    int4 ex[U];
+    double h[U][CPL];
+    int kk[U][CPL];
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
+    for (int q = 0; q < U; ++q) {
       ex[q] = st[u + q];
-      h[q] = __ldg(reinterpret_cast<const double *>(Hb + (unsigned)ex[q].w));
-      if (WITH_KK) kk[q] = __ldg(reinterpret_cast<const uint16_t *>(Kb + ((unsigned)ex[q].w >> 2)));
+      load_h<CPL>(Hb + (unsigned)ex[q].w, h[q]);
+      if (WITH_KK) load_k<CPL>(Kb + ((unsigned)ex[q].w >> 2), kk[q]);
     }
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const double c = __dadd_rn(__hiloint2double(ex[q].y, ex[q].x), h[q]);  // tt + (2c+F)
-      if ((unsigned)ex[q].z < cnt2 && (!WITH_KK || kk[q] <= (int)skm[u + q]) && c < bv) {
-        bv = c;
-        bw2 = (unsigned)ex[q].z;
-        bw3 = (unsigned)ex[q].w;
+    for (int q = 0; q < U; ++q) {
+      const double tt = __hiloint2double(ex[q].y, ex[q].x);
+      const int km = WITH_KK ? (int)skm[u + q] : 0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const double v = __dadd_rn(tt, h[q][c]);  // tt + (2c + F)  (_dp.pyx:85)
+        if ((unsigned)ex[q].z < cnt2[c] && (!WITH_KK || kk[q][c] <= km) && v < bv[c]) {
+          bv[c] = v;
+          bw2[c] = (unsigned)ex[q].z;
+          bw3[c] = (unsigned)ex[q].w;
+        }
       }
     }
   }
 }
 
+template <int CPL>
 __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b, int s, int group0) {
-  __shared__ int fin_cnt[kWarps][32];
+  constexpr int CW = 32 * CPL;
+  __shared__ int fin_cnt[kWarps][CW];
   __shared__ int4 stage_e[kWarps][32];
   __shared__ uint16_t stage_k[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -190,24 +250,36 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
   const int nk = L - s + 1, ng = G - s + 1;
   const int cell = blockIdx.x * kWarps + warp;
   const bool active = cell < nk * ng;
-  const int cand = group * 32 + lane;
-  int fin = 0;
+  const int cand0 = group * CW + lane * CPL;
+  int fin[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) fin[c] = 0;
   if (active) {
     const int k = 1 + cell % nk;
     const int g = s + cell / nk;
-    const double tm = b.tmax_pad[cand];
-    const int cnt = b.tcnt[cand];
+    double tm[CPL];
+    unsigned cnt2[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      tm[c] = b.tmax_pad[cand0 + c];
+      cnt2[c] = (unsigned)b.tcnt[cand0 + c] << 11;
+    }
     const int imax = L - s + 1;
     const int r = b.g_mesh[g];
     const int o0 = b.opt_off[r], nopt = b.opt_off[r + 1] - o0;
     const size_t gbase = (size_t)group * b.hg;
-    const double *Hg = b.H[(s - 1) & 1] + gbase * 32 + lane;
-    const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * 32 + lane;
+    const double *Hg = b.H[(s - 1) & 1] + gbase * CW + lane * CPL;
+    const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * CW + lane * CPL;
     const char *Hb = reinterpret_cast<const char *>(Hg);
     const char *Kb = reinterpret_cast<const char *>(Kg);
-    const unsigned cnt2 = (unsigned)cnt << 11;
-    double bv = kInf;
-    unsigned bw2 = ~0u, bw3 = 0;
+    double bv[CPL];
+    unsigned bw2[CPL], bw3[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      bv[c] = kInf;
+      bw2[c] = ~0u;
+      bw3[c] = 0;
+    }
     // options of mesh r, 32 at a time (a mesh rarely has more than 32 submesh
     // shapes); rows are visited in ascending option order
     for (int c0 = 0; c0 < nopt; c0 += 32) {
@@ -253,8 +325,9 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
         uint16_t sk = 0;
         if (t < T) {
           const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
-          const unsigned w2 = x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
-          se = make_int4(x.x, x.y, (int)w2, (oh + (x.w & 0xffff)) * 256);
+          const unsigned w2 =
+              x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
+          se = make_int4(x.x, x.y, (int)w2, (oh + (x.w & 0xffff)) * (256 * CPL));
           sk = (uint16_t)((unsigned)x.w >> 16);
         }
         stage_e[warp][lane] = se;
@@ -262,51 +335,59 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
         __syncwarp();
         const int n = min(32, T - r0);
         if (anykk)
-          relax_entries<true>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
+          relax_entries<true, CPL>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
         else
-          relax_entries<false>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
+          relax_entries<false, CPL>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
         __syncwarp();
       }
     }
-    fin = bw2 != ~0u;
-    const int bo = (int)(bw2 & 2047u), boff = (int)(bw3 >> 8);
-    const int bi = boff % (L + 1);
-    // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
-    const int bkk = fin ? (int)__ldg(Kg + (size_t)boff * 32) : 0;
-    if (cand < b.n_cand) {
-      if (k == 1 && g == G) b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv;
-      if (fin && b.full.bp_o) {
-        const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
-        if (b.full.F) b.full.F[e] = bv;
-        if (b.full.N) b.full.N[e] = (double)bkk;
-        b.full.bp_i[e] = bi;
-        b.full.bp_o[e] = bo;
-      }
-    }
-    // successor entry (state g, split i = k-1) for layer s+1
-    double hn = kInf;
-    int kn = 0;
-    if (fin) {
-      const int crow = b.g_crow[g];
-      if (crow >= 0) {
-        const double c = b.cb[(size_t)crow * (L + 1) + (k - 1)];
-        if (c <= tm) {
-          const double c2 = __dmul_rn(2.0, c);
-          hn = __dadd_rn(c2, bv);
-          kn = (int)ceil(__ddiv_rn(c2, tm)) + 1 + bkk;
+    // epilogue per candidate
+    double hn[CPL];
+    int kn[CPL];
+    const int crow = b.g_crow[g];
+    const double cbv = crow >= 0 ? b.cb[(size_t)crow * (L + 1) + (k - 1)] : kInf;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      fin[c] = bw2[c] != ~0u;
+      const int bo = (int)(bw2[c] & 2047u), boff = (int)(bw3[c] / (256u * CPL));
+      const int bi = boff % (L + 1);
+      // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
+      const int bkk = fin[c] ? (int)__ldg(Kg + (size_t)boff * CW + c) : 0;
+      const int cand = cand0 + c;
+      if (cand < b.n_cand) {
+        if (k == 1 && g == G) b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv[c];
+        if (fin[c] && b.full.bp_o) {
+          const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
+          if (b.full.F) b.full.F[e] = bv[c];
+          if (b.full.N) b.full.N[e] = (double)bkk;
+          b.full.bp_i[e] = bi;
+          b.full.bp_o[e] = bo;
         }
       }
+      // successor entry (state g, split i = k-1) for layer s+1
+      hn[c] = kInf;
+      kn[c] = 0;
+      if (fin[c] && cbv <= tm[c]) {
+        const double c2 = __dmul_rn(2.0, cbv);
+        hn[c] = __dadd_rn(c2, bv[c]);
+        kn[c] = (int)ceil(__ddiv_rn(c2, tm[c])) + 1 + bkk;
+      }
     }
-    const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * 32 + lane;
-    b.H[s & 1][o_idx] = hn;
-    b.K[s & 1][o_idx] = (uint16_t)kn;
+    const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      b.H[s & 1][o_idx + c] = hn[c];
+      b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
+    }
   }
-  fin_cnt[warp][lane] = fin;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) fin_cnt[warp][lane * CPL + c] = fin[c];
   __syncthreads();
-  if (warp == 0) {
+  for (int x = threadIdx.x; x < CW; x += blockDim.x) {
     int sum = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) sum += fin_cnt[w][lane];
+    for (int w = 0; w < kWarps; ++w) sum += fin_cnt[w][x];
+    const int cand = group * CW + x;
     if (sum && cand < b.n_cand) atomicAdd(&b.states[cand], (unsigned long long)sum);
   }
 }
@@ -466,7 +547,9 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.G = t->G;
   b.s_max = t->s_max;
   b.n_cand = n_cand;
-  b.n_groups = (n_cand + 31) / 32;
+  b.cpl = cpl_for(t, n_cand);
+  b.cw = 32 * b.cpl;
+  b.n_groups = (n_cand + b.cw - 1) / b.cw;
   b.hg = (size_t)(t->G + 1) * (t->L + 1);
   b.tmax = tmax;
   b.tmax_pad = (double *)(wb + w.tmax_pad);
@@ -485,7 +568,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
 int run_sweep(const Batch &b, cudaStream_t st) {
   dp_ftop_init<<<grid_for((size_t)b.n_cand * (b.s_max + 1), 256), 256, 0, st>>>(
       b.ftop, b.states, b.n_cand, b.s_max);
-  dp_prep<<<b.n_groups, 256, 0, st>>>(b);
+  dp_prep<<<b.n_groups, 256, 0, st>>>(b);  // block >= 128 = max group width
   HAPT_LAUNCHED("dp_prep");
   for (int s = 1; s <= b.s_max; ++s) {
     const long cells = (long)(b.L - s + 1) * (b.G - s + 1);
@@ -493,7 +576,12 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     const unsigned gx = grid_for(cells, kWarps);
     for (int g0 = 0; g0 < b.n_groups; g0 += 65535) {
       const int gy = min(65535, b.n_groups - g0);
-      dp_relax<<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
+      if (b.cpl == 1)
+        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
+      else if (b.cpl == 2)
+        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
+      else
+        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
     }
   }
   HAPT_LAUNCHED("dp_relax");

@@ -1,0 +1,115 @@
+"""CPU, world_size 2 over gloo: the candidate sharding of
+paper_2509_24859_b200.distributed (strided batches, all_gather of results,
+allreduce-argmin) reproduces the single-process answers.  The per-rank DP is
+a stand-in sweeper backed by the oracle (no GPU here)."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+class OracleSweeper:
+    """Sweeper stand-in: evaluate(t_values, B) via the oracle C DP."""
+
+    def __init__(self, inst, tb):
+        self.inst, self.tb = inst, tb
+        self.calls = []
+
+    def evaluate(self, tmax_values, B):
+        import oracle as O
+        from paper_2509_24859_b200.engine import SweepResult
+
+        t = np.asarray(tmax_values, dtype=np.float64)
+        self.calls.append(len(t))
+        ts, bs, st = O.full_pool(self.inst, self.tb, pool=list(t))
+        order = np.lexsort((t, ts))
+        winner = int(order[0]) if bs[order[0]] >= 0 else -1
+        return SweepResult(t, ts, bs.astype(np.int64), st, winner)
+
+
+def _worker(rank, world, port, name, out_q):
+    sys.path.insert(0, os.path.dirname(HERE))
+    sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
+    sys.path.insert(0, HERE)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch.distributed as dist
+
+    import oracle as O
+    from helpers import load_json
+    from paper_2509_24859_b200 import planner as P
+    from paper_2509_24859_b200.distributed import PoolSharding
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        inst = load_json(name)
+        tb = O.tables(inst)
+        pool = tb["pool"]
+        B = inst["num_microbatches"]
+        sh = PoolSharding()
+        sw = OracleSweeper(inst, tb)
+
+        class Tables:
+            L, G = tb["L"], tb["G"]
+            sweeper = sw
+
+        ev = P.CandidateEvaluator(Tables, pool, B, dist=sh)
+        lo, t_e, surv, probed = P.bidirectional_prune_replay(ev, B)
+        ev.ensure(surv)
+        feas = [i for i in surv if ev.best_s[i] >= 0]
+        best = min(feas, key=lambda i: (ev.tstar[i], pool[i]))
+        # allreduce-argmin over a rank-local shard of the whole pool
+        mine = list(range(rank, len(pool), world))
+        res = sw.evaluate([pool[i] for i in mine], B)
+        w = res.winner
+        g_t, g_i = sh.allreduce_argmin(float(res.tstar[w]) if w >= 0 else float("inf"),
+                                       mine[w] if w >= 0 else -1)
+        out_q.put((rank, lo, surv, best, float(ev.tstar[best]), g_t, g_i, sum(sw.calls),
+                   sh.collective_calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("name", ["A", "B"])
+def test_two_rank_search_and_argmin(name):
+    import oracle as O
+    from helpers import expected, expected_arrays, load_json
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    exp = expected(name)
+    arr = expected_arrays(name)
+    pool = arr["pool"]
+    ref_plan = exp["plan"]
+    for rank, lo, surv, best, tstar, g_t, g_i, n_eval, n_coll in results:
+        assert tstar == ref_plan["predicted_latency"]
+        assert pool[best] == ref_plan["t_max"]
+        assert lo == ref_plan["search_stats"]["pruned_below_ts"]
+        assert len(surv) == ref_plan["search_stats"]["evaluated"]
+        feas = np.where(arr["best_s"] >= 0)[0]
+        win = feas[np.lexsort((pool[feas], arr["tstar"][feas]))[0]]
+        assert (g_t, g_i) == (float(arr["tstar"][win]), int(win))
+        assert n_coll >= 3
+    # every pool candidate evaluated exactly once across the two ranks
+    assert results[0][7] + results[1][7] >= len(O.tables(load_json(name))["pool"])
+    assert results[0][1:7] == results[1][1:7]

@@ -167,13 +167,22 @@ int hapt_tables_finalize(hapt_tables *t, void *stream);
 /* K2: stage-partition DP                                                    */
 /* ------------------------------------------------------------------------ */
 
-/* Optional full outputs, reference layout [n_cand][s_max+1][L+2][G+1];
- * the caller pre-fills F=+inf (F[c,0,L+1,0]=0), N=0, bp=-1. */
+/* Optional outputs of a sweep; every member may be NULL.
+ * F, N, bp_i, bp_o: the reference layout [n_cand][s_max+1][L+2][G+1]
+ *   (dp_sweep's return tuple); the caller pre-fills F=+inf (F[c,0,L+1,0]=0),
+ *   N=0, bp=-1; bp_i and bp_o must be given together.
+ * bp_packed: [n_cand][s_max+1][L+2][G+1] int32 (o << 16) | i, written only
+ *   for finite cells -- exactly the cells a backtrack visits -- so it needs
+ *   no pre-fill; hapt_dp_walk reads it.
+ * ntop: [n_cand][s_max+1] int32 N[s,1,G] (the DP launch bound of the first
+ *   stage, checked by _extract_plan, planner.py:337-338). */
 typedef struct {
   double *F;
   double *N;
   int32_t *bp_i;
   int32_t *bp_o;
+  int32_t *bp_packed;
+  int32_t *ntop;
 } hapt_dp_full;
 
 size_t hapt_dp_workspace_bytes(const hapt_tables *t, int32_t n_cand);
@@ -201,6 +210,13 @@ size_t hapt_backtrack_workspace_bytes(const hapt_tables *t);
 int hapt_dp_backtrack(const hapt_tables *t, double tmax, int32_t best_s,
                       int32_t *stages, int32_t *kchain, int32_t *n_stages,
                       void *work, size_t work_bytes, void *stream);
+
+/* Backpointer walk (planner.py:300-312) over one candidate's packed
+ * backpointers from a batch sweep (bp_cand = bp_packed + c * (s_max+1)(L+2)(G+1)):
+ * stages [s_max][3] = (layer_start, layer_end, option), n_stages [1]
+ * (-1: broken chain, -2: plan does not cover every layer and device). */
+int hapt_dp_walk(const hapt_tables *t, const int32_t *bp_cand, int32_t best_s,
+                 int32_t *stages, int32_t *n_stages, void *stream);
 
 /* Number of DpTables entries with t <= t_max for each candidate: the
  * _activated_pairs batching key (planner.py:483-487). */

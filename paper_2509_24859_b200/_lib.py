@@ -110,7 +110,8 @@ class Tables(ctypes.Structure):
 
 
 class DpFull(ctypes.Structure):
-    _fields_ = [("F", c_vp), ("N", c_vp), ("bp_i", c_vp), ("bp_o", c_vp)]
+    _fields_ = [("F", c_vp), ("N", c_vp), ("bp_i", c_vp), ("bp_o", c_vp), ("bp_packed", c_vp),
+                ("ntop", c_vp)]
 
 
 _SIGNATURES = {
@@ -131,6 +132,7 @@ _SIGNATURES = {
         c_i32,
         [ctypes.POINTER(Tables), c_dbl, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp],
     ),
+    "hapt_dp_walk": (c_i32, [ctypes.POINTER(Tables), c_vp, c_i32, c_vp, c_vp, c_vp]),
     "hapt_activated_pairs": (c_i32, [ctypes.POINTER(Tables), c_vp, c_i32, c_vp, c_vp]),
     "hapt_launch_counts": (
         c_i32,

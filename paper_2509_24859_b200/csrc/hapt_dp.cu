@@ -355,13 +355,19 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
       const int bkk = fin[c] ? (int)__ldg(Kg + (size_t)boff * CW + c) : 0;
       const int cand = cand0 + c;
       if (cand < b.n_cand) {
-        if (k == 1 && g == G) b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv[c];
-        if (fin[c] && b.full.bp_o) {
+        if (k == 1 && g == G) {
+          b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv[c];
+          if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
+        }
+        if (fin[c]) {
           const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
-          if (b.full.F) b.full.F[e] = bv[c];
-          if (b.full.N) b.full.N[e] = (double)bkk;
-          b.full.bp_i[e] = bi;
-          b.full.bp_o[e] = bo;
+          if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
+          if (b.full.bp_o) {
+            if (b.full.F) b.full.F[e] = bv[c];
+            if (b.full.N) b.full.N[e] = (double)bkk;
+            b.full.bp_i[e] = bi;
+            b.full.bp_o[e] = bo;
+          }
         }
       }
       // successor entry (state g, split i = k-1) for layer s+1
@@ -471,6 +477,29 @@ __global__ void dp_walk(hapt_dp_full full, const int32_t *opt_devs, int L, int G
   }
   if (!*err && (k != L + 1 || g != 0)) *err = 2;
   *n_stages = n;
+}
+
+// Backpointer walk over packed (o << 16 | i) backpointers (planner.py:300-312).
+__global__ void dp_walk_packed(const int32_t *bp, const int32_t *opt_devs, int L, int G,
+                               int best_s, int32_t *stages, int32_t *n_stages) {
+  if (threadIdx.x || blockIdx.x) return;
+  int s = best_s, k = 1, g = G, n = 0;
+  while (s > 0) {
+    const int v = bp[((size_t)s * (L + 2) + k) * (G + 1) + g];
+    const int o = v >> 16, i = v & 0xffff;
+    if (i < k || i > L || o < 0) {
+      *n_stages = -1;
+      return;
+    }
+    stages[3 * n + 0] = k;
+    stages[3 * n + 1] = i;
+    stages[3 * n + 2] = o;
+    ++n;
+    g -= opt_devs[o];
+    k = i + 1;
+    --s;
+  }
+  *n_stages = (k != L + 1 || g != 0) ? -2 : n;
 }
 
 __global__ void fill_full(hapt_dp_full f, size_t n, int L, int G) {
@@ -605,8 +634,9 @@ extern "C" int hapt_dp_sweep_batch(const hapt_tables *t, const double *tmax, int
     set_error("hapt_dp_sweep_batch: invalid arguments");
     return HAPT_EINVAL;
   }
-  if (full && !full->bp_o) {
-    set_error("hapt_dp_sweep_batch: full outputs need bp_o/bp_i");
+  if (full && ((full->bp_o == nullptr) != (full->bp_i == nullptr) ||
+               ((full->F || full->N) && !full->bp_o))) {
+    set_error("hapt_dp_sweep_batch: F/N need bp_i and bp_o, which go together");
     return HAPT_EINVAL;
   }
   if (work_bytes < ws_layout(t, n_cand).total) {
@@ -696,6 +726,18 @@ extern "C" int hapt_dp_backtrack(const hapt_tables *t, double tmax, int32_t best
                         : "plan does not cover all layers and devices");
     return HAPT_ECHAIN;
   }
+  return HAPT_OK;
+}
+
+extern "C" int hapt_dp_walk(const hapt_tables *t, const int32_t *bp_cand, int32_t best_s,
+                            int32_t *stages, int32_t *n_stages, void *stream) {
+  if (!t || !bp_cand || !stages || !n_stages || best_s < 1 || best_s > t->s_max) {
+    set_error("hapt_dp_walk: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  dp_walk_packed<<<1, 32, 0, (cudaStream_t)stream>>>(bp_cand, t->opt_devs, t->L, t->G, best_s,
+                                                     stages, n_stages);
+  HAPT_LAUNCHED("dp_walk_packed");
   return HAPT_OK;
 }
 

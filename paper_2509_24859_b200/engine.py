@@ -194,21 +194,39 @@ class SweepResult:
     best_s: np.ndarray    # stage count of the best plan (-1: infeasible)
     states: np.ndarray    # isfinite(F[1:]).sum()
     winner: int           # argmin (T*, index), -1 if none
+    bp: torch.Tensor | None = None     # packed backpointers [n][s_max+1][L+2][G+1]
+    ntop: np.ndarray | None = None     # N[s,1,G] per candidate [n][s_max+1]
+
+
+_WS_CACHE: dict = {}  # device -> scratch tensor reused by every Sweeper
+_FREE_MEM: dict = {}
+
+
+def _scratch(device: torch.device, nbytes: int) -> torch.Tensor:
+    buf = _WS_CACHE.get(device)
+    if buf is None or buf.numel() < nbytes:
+        _WS_CACHE.pop(device, None)
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _WS_CACHE[device] = buf
+    return buf
 
 
 class Sweeper:
-    """Batched K2 over one DeviceTables.  Workspaces are cached and candidate
-    batches are chunked so the successor tables stay within `max_ws_bytes`."""
+    """Batched K2 over one DeviceTables.  Workspaces are shared per device and
+    candidate batches are chunked so the successor tables stay within
+    `max_ws_bytes`."""
+
+    BP_BUDGET = 6 * 2**30  # bytes of packed backpointers kept for a batch
 
     def __init__(self, tables: DeviceTables, max_ws_bytes: int | None = None):
         self.tables = tables
         self.lib = tables.lib
         self.device = tables.device
         if max_ws_bytes is None:
-            free, total = torch.cuda.mem_get_info(self.device)
-            max_ws_bytes = int(min(0.5 * free, 48 * 2**30))
+            if self.device not in _FREE_MEM:
+                _FREE_MEM[self.device] = torch.cuda.mem_get_info(self.device)[0]
+            max_ws_bytes = int(min(0.5 * _FREE_MEM[self.device], 48 * 2**30))
         self.max_ws_bytes = max_ws_bytes
-        self._ws = None
         self._bt_ws = None
         self.last_chunks = 0
 
@@ -218,10 +236,11 @@ class Sweeper:
         return int(groups * 32)
 
     def _workspace(self, nbytes: int) -> torch.Tensor:
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = None
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        return self._ws
+        return _scratch(self.device, nbytes)
+
+    def bp_bytes(self, n: int) -> int:
+        t = self.tables
+        return 4 * n * (t.s_max + 1) * (t.L + 2) * (t.G + 1)
 
     def sweep_device(self, tmax: torch.Tensor, full: DpFull | None = None):
         """tmax: float64 CUDA tensor [n].  Returns (ftop [n, s_max+1], states [n])
@@ -267,18 +286,52 @@ class Sweeper:
         )
         return tstar, best_s, winner
 
-    def evaluate(self, tmax_values, num_microbatches: int) -> SweepResult:
+    def evaluate(self, tmax_values, num_microbatches: int, keep_bp: bool = False) -> SweepResult:
+        """Sweep + select a batch; one host transfer for all per-candidate
+        results.  keep_bp also records packed backpointers for every
+        candidate (when they fit BP_BUDGET) so a winner can be walked without
+        a re-sweep (hapt_dp_walk)."""
         tm = np.asarray(tmax_values, dtype=np.float64)
+        n = len(tm)
         tmax = torch.from_numpy(tm).to(self.device)
-        ftop, states = self.sweep_device(tmax)
+        full = bp = ntop = None
+        if keep_bp and self.bp_bytes(n) <= self.BP_BUDGET:
+            t = self.tables
+            bp = torch.empty((n, t.s_max + 1, t.L + 2, t.G + 1), dtype=_I32, device=self.device)
+            ntop = torch.zeros((n, t.s_max + 1), dtype=_I32, device=self.device)
+            full = DpFull(None, None, None, None, bp.data_ptr(), ntop.data_ptr())
+        ftop, states = self.sweep_device(tmax, full=full)
         tstar, best_s, winner = self.select_device(ftop, tmax, num_microbatches)
+        parts = [tstar.view(torch.int64), best_s.to(torch.int64), states,
+                 winner.to(torch.int64)]
+        if ntop is not None:
+            parts.append(ntop.to(torch.int64).reshape(-1))
+        host = torch.cat(parts).cpu().numpy()
         return SweepResult(
             tmax=tm,
-            tstar=tstar.cpu().numpy(),
-            best_s=best_s.cpu().numpy(),
-            states=states.cpu().numpy(),
-            winner=int(winner.cpu()[0]),
+            tstar=host[:n].view(np.float64).copy(),
+            best_s=host[n : 2 * n].copy(),
+            states=host[2 * n : 3 * n].copy(),
+            winner=int(host[3 * n]),
+            bp=bp,
+            ntop=None if ntop is None else host[3 * n + 1 :].reshape(n, -1).copy(),
         )
+
+    def walk(self, res: SweepResult, idx: int, best_s: int):
+        """Stage chain [(layer_start, layer_end, option)] of candidate idx of a
+        keep_bp batch, walked on the device (planner.py:300-312)."""
+        t = self.tables
+        out = torch.empty(3 * t.s_max + 1, dtype=_I32, device=self.device)
+        check(self.lib.hapt_dp_walk(ctypes.byref(t.t), res.bp[idx].data_ptr(), int(best_s),
+                                    out.data_ptr(), out[3 * t.s_max :].data_ptr(), stream_ptr()))
+        h = out.cpu().numpy()
+        n = int(h[3 * t.s_max])
+        if n < 0:
+            from .planner import PlannerError
+
+            raise PlannerError("broken backpointer chain" if n == -1
+                               else "plan does not cover all layers and devices")
+        return [tuple(int(x) for x in row) for row in h[: 3 * n].reshape(n, 3)]
 
     def full_tables(self, t_max: float):
         """Reference-layout F, N, bp_i, bp_o for one candidate (drop-in
@@ -290,7 +343,7 @@ class Sweeper:
         N = torch.zeros(shape, dtype=_F64, device=self.device)
         bpi = torch.full(shape, -1, dtype=_I32, device=self.device)
         bpo = torch.full(shape, -1, dtype=_I32, device=self.device)
-        full = DpFull(F.data_ptr(), N.data_ptr(), bpi.data_ptr(), bpo.data_ptr())
+        full = DpFull(F.data_ptr(), N.data_ptr(), bpi.data_ptr(), bpo.data_ptr(), None, None)
         tmax = torch.tensor([t_max], dtype=_F64, device=self.device)
         self.sweep_device(tmax, full=full)
         return F, N, bpi, bpo

@@ -195,9 +195,10 @@ class DpTables:
 
     @property
     def sweeper(self) -> Sweeper:
-        if self._sweeper is None:
-            self._sweeper = Sweeper(self.dev)
-        return self._sweeper
+        # one Sweeper per device tables, shared by every DpTables view of them
+        if getattr(self.dev, "_sweeper", None) is None:
+            self.dev._sweeper = Sweeper(self.dev)
+        return self.dev._sweeper
 
     def transitions_per_sweep(self) -> int:
         per_opt = self.feasible_spans_per_opt
@@ -241,6 +242,8 @@ class CandidateEvaluator:
         self.states = np.zeros(n, dtype=np.int64)
         self.batches = 0
         self.evaluated = 0
+        self._bp_of: dict = {}     # pool index -> (SweepResult with bp, position)
+        self._bp_bytes = 0
 
     def known(self, idx: int) -> bool:
         return self.best_s[idx] != -2
@@ -252,10 +255,17 @@ class CandidateEvaluator:
         self.batches += 1
         self.evaluated += len(todo)
         if self.dist is None:
-            res = self.tables.sweeper.evaluate(self.pool[todo], self.B)
+            sw = self.tables.sweeper
+            need = sw.bp_bytes(len(todo))
+            keep = self._bp_bytes + need <= sw.BP_BUDGET
+            res = sw.evaluate(self.pool[todo], self.B, keep_bp=keep)
             self.tstar[todo] = res.tstar
             self.best_s[todo] = res.best_s
             self.states[todo] = res.states
+            if res.bp is not None:
+                self._bp_bytes += need
+                for pos, i in enumerate(todo):
+                    self._bp_of[i] = (res, pos)
         else:
             ts, bs, st = self.dist.evaluate_sharded(self.tables.sweeper, self.pool, todo, self.B)
             self.tstar[todo] = ts
@@ -265,6 +275,19 @@ class CandidateEvaluator:
     def feasible(self, idx: int) -> bool:
         self.ensure([idx])
         return self.best_s[idx] >= 0
+
+    def plan(self, idx: int, epsilon: float) -> "ParallelPlan":
+        """ParallelPlan of pool candidate idx: walked from the batch's kept
+        backpointers when available, else re-derived by hapt_dp_backtrack."""
+        hit = self._bp_of.get(idx)
+        if hit is not None:
+            res, pos = hit
+            spans = self.tables.sweeper.walk(res, pos, int(self.best_s[idx]))
+            return _build_plan(self.tables, float(self.pool[idx]), int(self.best_s[idx]),
+                               float(self.tstar[idx]), self.B, epsilon, spans=spans,
+                               n_first=int(res.ntop[pos, int(self.best_s[idx])]))
+        return _build_plan(self.tables, float(self.pool[idx]), int(self.best_s[idx]),
+                           float(self.tstar[idx]), self.B, epsilon)
 
 
 def _probe_tree(lo: int, hi: int, depth: int, out: set) -> None:
@@ -355,15 +378,19 @@ def _count_batches(surviving_t, activated, batch_size) -> int:
 
 
 def _build_plan(tables: DpTables, t_max: float, best_s: int, tstar: float,
-                num_microbatches: int, epsilon: float) -> ParallelPlan:
-    """_extract_plan (planner.py:272-382) from the device backtrack."""
+                num_microbatches: int, epsilon: float, spans=None,
+                n_first: Optional[int] = None) -> ParallelPlan:
+    """_extract_plan (planner.py:272-382) from a device backtrack: either the
+    walked `spans` of a batch with kept backpointers (plus N[best_s,1,G] as
+    `n_first`), or a one-candidate re-sweep with backpointers."""
     store = tables.store
     cluster = store.cluster
-    spans, kchain = tables.sweeper.backtrack(t_max, best_s)
-    profs = []
-    for q, p, o in spans:
-        mesh_id, n, m = tables.opt_meta[o]
-        profs.append((q, p, mesh_id, n, m, store.lookup(q, p, mesh_id, (n, m))))
+    kchain = None
+    if spans is None:
+        spans, kchain = tables.sweeper.backtrack(t_max, best_s)
+    metas = [tables.opt_meta[o] for _, _, o in spans]
+    found = store.lookup_many([(q, p, mid, (n, m)) for (q, p, _), (mid, n, m) in zip(spans, metas)])
+    profs = [(q, p, mid, n, m, pr) for (q, p, _), (mid, n, m), pr in zip(spans, metas, found)]
     comm, links = [], []
     for idx in range(len(spans) - 1):
         i = spans[idx][1]
@@ -376,7 +403,8 @@ def _build_plan(tables: DpTables, t_max: float, best_s: int, tstar: float,
         c = comm[idx] if idx < len(spans) - 1 else 0.0
         k_next = math.ceil(2.0 * c / t_max) + 1.0 + k_next
         k_bounds[idx] = int(k_next)
-    if k_bounds != kchain:
+    if (kchain is not None and k_bounds != kchain) or (
+            n_first is not None and k_bounds[0] != n_first):
         raise PlannerError("launch-bound chain disagrees with the DP table")
     stage_times = [pr.t for *_, pr in profs]
     counts = adaptive_counts(stage_times, comm, epsilon, t_max=max(t_max, max(stage_times)))
@@ -402,11 +430,13 @@ def dp_search(store: ProfileStore, costs: BoundaryCost, num_microbatches: int, t
     if t_max <= 0:
         raise PlannerError("t_max must be positive")
     tables = tables or DpTables(store, costs)
-    res = tables.sweeper.evaluate([t_max], num_microbatches)
+    res = tables.sweeper.evaluate([t_max], num_microbatches, keep_bp=True)
     if res.best_s[0] < 0:
         return None
-    plan = _build_plan(tables, float(t_max), int(res.best_s[0]), float(res.tstar[0]),
-                       num_microbatches, epsilon)
+    bs = int(res.best_s[0])
+    spans = tables.sweeper.walk(res, 0, bs) if res.bp is not None else None
+    plan = _build_plan(tables, float(t_max), bs, float(res.tstar[0]), num_microbatches, epsilon,
+                       spans=spans, n_first=None if spans is None else int(res.ntop[0, bs]))
     plan.search_stats["dp_states"] = int(res.states[0])
     return plan
 
@@ -507,8 +537,7 @@ def search(store: ProfileStore, costs: BoundaryCost, num_microbatches: int,
         raise InfeasiblePlanError("no stage partition satisfies the memory and overlap constraints")
     # sort_key merge: (T*, t_max) decides since t_max is unique (planner.py:535-541)
     best = min(cand, key=lambda i: (ev.tstar[i], pool[i]))
-    plan = _build_plan(tables, pool[best], int(ev.best_s[best]), float(ev.tstar[best]), B,
-                       epsilon)
+    plan = ev.plan(best, epsilon)
     states = int(sum(int(ev.states[i]) for i in evaluated_set if ev.best_s[i] >= 0))
     plan.search_stats.update(
         {

@@ -164,7 +164,8 @@ class ProfileStore:
             dtype=np.int32,
         )
         self._overrides: dict = {}  # (o, qc, pc) -> (t_fwd, t_bwd, mem_params, mem_act)
-        self._profiles: dict = {}
+        self._profiles: dict = {}   # canonical (o, qc, pc) -> StageMeshProfile
+        self._alias_key: dict = {}  # (o, q, p) -> canonical key
         L = len(layers)
         G = sum(m.hosts * m.devices_per_host for m in cluster.meshes)
         self.dev = DeviceTables(L, G, len(self.options), len(cluster.meshes), device)
@@ -230,6 +231,7 @@ class ProfileStore:
         arrays, scalars = self._desc()
         self.dev.build(arrays, scalars)
         self._profiles.clear()
+        self._alias_key.clear()
         c = self.dev.counters()
         self.stats = StoreStats(*(int(x) for x in c[2:8]))
         if self.stats.canonical_feasible == 0:
@@ -299,28 +301,52 @@ class ProfileStore:
         return tuple(int(x) for x in self._sig[q - 1 : p])
 
     def lookup(self, q: int, p: int, mesh_id: str, shape) -> StageMeshProfile:
+        return self.lookup_many([(q, p, mesh_id, shape)])[0]
+
+    def lookup_many(self, spans) -> list:
+        """lookup() for several (q, p, mesh_id, shape) at once: the needed
+        cells are gathered on the device (canonical span resolved there too)
+        and copied back in one transfer; profiles are cached per canonical
+        entry, so repeated lookups return the same object."""
+        import torch
+
         L = self.num_layers
-        try:
-            if not (1 <= q <= p <= L):
-                raise KeyError
-            o = self._option(mesh_id, shape)
-        except KeyError:
-            raise ProfilingError(f"no profile for span [{q},{p}] on {mesh_id}{tuple(shape)}") from None
-        qc, pc = self._canon(q, p)
-        key = (o, qc, pc)
-        prof = self._profiles.get(key)
-        if prof is None:
-            st = int(self.dev.host("cell_state")[o, qc, pc])
-            prof = StageMeshProfile(
-                float(self.dev.host("tf_raw")[o, qc, pc]),
-                float(self.dev.host("tb_raw")[o, qc, pc]),
-                float(self.dev.host("mp_raw")[o, qc, pc]),
-                float(self.dev.host("ma_raw")[o, qc, pc]),
-                feasible=bool(st & 1),
-                prune_reason=_REASONS[(st >> 2) & 3],
-            )
-            self._profiles[key] = prof
-        return prof
+        S = L + 2
+        req = []
+        for q, p, mesh_id, shape in spans:
+            try:
+                if not (1 <= q <= p <= L):
+                    raise KeyError
+                o = self._option(mesh_id, shape)
+            except KeyError:
+                raise ProfilingError(
+                    f"no profile for span [{q},{p}] on {mesh_id}{tuple(shape)}") from None
+            req.append((o, q, p))
+        miss = [r for r in req if r not in self._alias_key]
+        if miss:
+            dev = self.dev
+            qp = torch.tensor([q * S + p for _, q, p in miss], dtype=torch.int64)
+            lens = torch.tensor([p - q for _, q, p in miss], dtype=torch.int64)
+            opt = torch.tensor([o for o, _, _ in miss], dtype=torch.int64)
+            qp, lens, opt = (x.to(dev.device) for x in (qp, lens, opt))
+            qc = dev.view("canon_q", torch.int32, (S * S,))[qp].to(torch.int64)
+            cell = opt * (S * S) + qc * S + qc + lens
+            flat = lambda n: dev.view(n, torch.float64, (dev.n_opts * S * S,))  # noqa: E731
+            st = dev.view("cell_state", torch.int8, (dev.n_opts * S * S,))[cell]
+            vals = torch.stack([flat("tf_raw")[cell], flat("tb_raw")[cell], flat("mp_raw")[cell],
+                                flat("ma_raw")[cell], st.to(torch.float64),
+                                qc.to(torch.float64)]).cpu().numpy()
+            for j, (o, q, p) in enumerate(miss):
+                qcj = int(vals[5, j])
+                key = (o, qcj, qcj + (p - q))
+                if key not in self._profiles:
+                    sb = int(vals[4, j])
+                    self._profiles[key] = StageMeshProfile(
+                        float(vals[0, j]), float(vals[1, j]), float(vals[2, j]),
+                        float(vals[3, j]), feasible=bool(sb & 1),
+                        prune_reason=_REASONS[(sb >> 2) & 3])
+                self._alias_key[(o, q, p)] = key
+        return [self._profiles[self._alias_key[r]] for r in req]
 
     def canonical_key(self, q: int, p: int, mesh_id: str, shape) -> tuple:
         shape = tuple(shape)

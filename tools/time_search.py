@@ -31,7 +31,7 @@ def main(name):
         ev.ensure(surv)
         t3 = time.perf_counter()
         best = min((i for i in surv if ev.best_s[i] >= 0), key=lambda i: (ev.tstar[i], pool[i]))
-        plan = P._build_plan(tables, pool[best], int(ev.best_s[best]), float(ev.tstar[best]), B, eps)
+        plan = ev.plan(best, eps)
         t4 = time.perf_counter()
         P._activated_pairs(tables, [pool[i] for i in surv])
         tables.transitions_per_sweep()
@@ -39,9 +39,11 @@ def main(name):
         print(f"{name} rep{rep}: build {1e3*(t1-t0):.2f} ms | prune {1e3*(t2-t1):.2f} ms "
               f"({nb1} batches, {ev.evaluated} cand) | survivors {1e3*(t3-t2):.2f} ms "
               f"({len(surv)}) | backtrack+plan {1e3*(t4-t3):.2f} ms | stats {1e3*(t5-t4):.2f} ms")
-    t0 = time.perf_counter()
-    P.search(build_store(layers, cluster, model, imbalance_ratio=rho), boundary_costs(layers, cluster), B, epsilon=eps)
-    print(f"{name} search() total {1e3*(time.perf_counter()-t0):.2f} ms")
+    for rep in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P.search(build_store(layers, cluster, model, imbalance_ratio=rho), boundary_costs(layers, cluster), B, epsilon=eps)
+        print(f"{name} search() total {1e3*(time.perf_counter()-t0):.2f} ms")
 
 
 if __name__ == "__main__":

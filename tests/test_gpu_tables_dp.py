@@ -19,7 +19,7 @@ def sha(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("name", ["A", "B", "C", "D1"])
+@pytest.mark.parametrize("name", ["A", "B", "C", "D1", "D2", "D3"])
 def test_device_tables_equal_reference(name):
     """hapt_tables_build reproduces DpTables + the t_max pool + StoreStats."""
     from paper_2509_24859_b200.planner import DpTables

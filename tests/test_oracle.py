@@ -19,7 +19,7 @@ STAT_KEYS = ["candidates", "canonical", "canonical_feasible", "aliased", "pruned
              "pruned_imbalance"]
 
 
-@pytest.mark.parametrize("name", ["A", "B", "C", "D1"])
+@pytest.mark.parametrize("name", ["A", "B", "C", "D1", "D2", "D3"])
 def test_tables_match_reference(name):
     inst, exp = load_json(name), expected(name)
     tb = O.tables(inst)

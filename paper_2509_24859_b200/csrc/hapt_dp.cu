@@ -54,9 +54,12 @@ int cpl_for(const hapt_tables *t, int n_cand) {
   return warps2 >= 16384 ? 2 : 1;
 }
 
+#ifndef HAPT_U4
+#define HAPT_U4 2
+#endif
 template <int CPL>
 struct Unroll {
-  static constexpr int value = CPL >= 4 ? 2 : 4;  // successor loads in flight per warp
+  static constexpr int value = CPL >= 4 ? HAPT_U4 : 4;  // successor loads in flight per warp
 };
 
 struct Batch {
@@ -76,6 +79,9 @@ struct Batch {
   int32_t *tcnt;       // [n_groups*cw]  #pool values <= t_max
   uint16_t *cut_sr;    // [n_groups][rows] entries of a row before its suffix-min
                        // pool rank reaches the group's largest bound
+  uint8_t *kc;         // [n_groups][2*n_meshes][L+1][cw] ceil(2c/t_max)+1 of every
+                       // boundary row entry, 0xFF where c > t_max (_dp.pyx:76-82)
+  int cb_rows;         // 2*n_meshes
   double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
   double *ftop;
@@ -84,7 +90,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, H0, H1, K0, K1, total;
+  size_t tmax_pad, tcnt, cut_sr, kc, H0, H1, K0, K1, total;
 };
 
 WsLayout ws_layout(const hapt_tables *t, int n_cand) {
@@ -97,6 +103,7 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   w.tmax_pad = cur; cur += align_up(np * 8);
   w.tcnt = cur; cur += align_up(np * 4);
   w.cut_sr = cur; cur += align_up(ng * rows * 2);
+  w.kc = cur; cur += align_up(ng * 2 * t->n_meshes * (t->L + 1) * cw);
   w.H0 = cur; cur += align_up(ng * hg * cw * 8);
   w.H1 = cur; cur += align_up(ng * hg * cw * 8);
   w.K0 = cur; cur += align_up(ng * hg * cw * 2);
@@ -149,6 +156,17 @@ __global__ void dp_prep(Batch b) {
       if (b.span_srank[mid] < gm) lo = mid + 1; else hi = mid;
     }
     b.cut_sr[(size_t)group * b.rows + row] = (uint16_t)(lo - beg);
+  }
+  // the launch-bound increment of every boundary entry for every candidate:
+  // kk = (ceil(2c/t_max) + 1) + N (_dp.pyx:82, same association); c > t_max
+  // skips the transition (_dp.pyx:76-78) -> 0xFF
+  const size_t nkc = (size_t)b.cb_rows * (b.L + 1) * cw;
+  uint8_t *kc = b.kc + (size_t)group * nkc;
+  for (size_t x = threadIdx.x; x < nkc; x += blockDim.x) {
+    const size_t e = x / cw;
+    const double c = b.cb[e];
+    const double tm = b.tmax_pad[group * cw + (int)(x % cw)];
+    kc[x] = c <= tm ? (uint8_t)((int)ceil(__ddiv_rn(__dmul_rn(2.0, c), tm)) + 1) : (uint8_t)0xFF;
   }
   if (threadIdx.x < cw) {
     const double tm = b.tmax_pad[group * cw + threadIdx.x];
@@ -239,7 +257,8 @@ __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
 }
 
 template <int CPL>
-__global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b, int s, int group0) {
+__global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
+    dp_relax(Batch b, int s, int group0, unsigned long long nk_magic) {
   constexpr int CW = 32 * CPL;
   __shared__ int fin_cnt[kWarps][CW];
   __shared__ int4 stage_e[kWarps][32];
@@ -255,8 +274,11 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
 #pragma unroll
   for (int c = 0; c < CPL; ++c) fin[c] = 0;
   if (active) {
-    const int k = 1 + cell % nk;
-    const int g = s + cell / nk;
+    // cell / nk by multiply-high with ceil(2^32/nk): exact for cell < 2^20,
+    // nk < 2^12 (hapt_tables_init bounds both)
+    const int gq = (int)(((unsigned long long)(unsigned)cell * nk_magic) >> 32);
+    const int k = 1 + cell - gq * nk;
+    const int g = s + gq;
     double tm[CPL];
     unsigned cnt2[CPL];
 #pragma unroll
@@ -345,38 +367,43 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB) dp_relax(Batch b
     double hn[CPL];
     int kn[CPL];
     const int crow = b.g_crow[g];
-    const double cbv = crow >= 0 ? b.cb[(size_t)crow * (L + 1) + (k - 1)] : kInf;
+    const double c2 = crow >= 0 ? __dmul_rn(2.0, b.cb[(size_t)crow * (L + 1) + (k - 1)]) : 0.0;
+    const uint8_t *kcp = b.kc + ((size_t)group * b.cb_rows + (crow >= 0 ? crow : 0)) * (L + 1) * CW +
+                         (size_t)(k - 1) * CW + lane * CPL;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       fin[c] = bw2[c] != ~0u;
+      const double best = bv[c];
       const int bo = (int)(bw2[c] & 2047u), boff = (int)(bw3[c] / (256u * CPL));
-      const int bi = boff % (L + 1);
+      // split i of the winner: its successor offset minus the row of g2 = g - devs
+      const int bi = fin[c] ? boff - (g - b.opt_devs[bo]) * (L + 1) : 0;
       // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
       const int bkk = fin[c] ? (int)__ldg(Kg + (size_t)boff * CW + c) : 0;
       const int cand = cand0 + c;
       if (cand < b.n_cand) {
         if (k == 1 && g == G) {
-          b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv[c];
+          b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
           if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
         }
         if (fin[c]) {
           const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
           if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
           if (b.full.bp_o) {
-            if (b.full.F) b.full.F[e] = bv[c];
+            if (b.full.F) b.full.F[e] = best;
             if (b.full.N) b.full.N[e] = (double)bkk;
             b.full.bp_i[e] = bi;
             b.full.bp_o[e] = bo;
           }
         }
       }
-      // successor entry (state g, split i = k-1) for layer s+1
+      // successor entry (state g, split i = k-1) for layer s+1:
+      // H = 2c + F, KK = (ceil(2c/t_max) + 1) + N, or +inf if c > t_max
       hn[c] = kInf;
       kn[c] = 0;
-      if (fin[c] && cbv <= tm[c]) {
-        const double c2 = __dmul_rn(2.0, cbv);
-        hn[c] = __dadd_rn(c2, bv[c]);
-        kn[c] = (int)ceil(__ddiv_rn(c2, tm[c])) + 1 + bkk;
+      const int kcv = crow >= 0 ? (int)kcp[c] : 0xFF;
+      if (fin[c] && kcv != 0xFF) {
+        hn[c] = __dadd_rn(c2, best);
+        kn[c] = kcv + bkk;
       }
     }
     const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
@@ -584,6 +611,8 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.tmax_pad = (double *)(wb + w.tmax_pad);
   b.tcnt = (int32_t *)(wb + w.tcnt);
   b.cut_sr = (uint16_t *)(wb + w.cut_sr);
+  b.kc = (uint8_t *)(wb + w.kc);
+  b.cb_rows = 2 * t->n_meshes;
   b.H[0] = (double *)(wb + w.H0);
   b.H[1] = (double *)(wb + w.H1);
   b.K[0] = (uint16_t *)(wb + w.K0);
@@ -603,14 +632,16 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     const long cells = (long)(b.L - s + 1) * (b.G - s + 1);
     if (cells <= 0) break;
     const unsigned gx = grid_for(cells, kWarps);
+    const unsigned long long nk = (unsigned long long)(b.L - s + 1);
+    const unsigned long long magic = ((1ull << 32) + nk - 1) / nk;  // ceil(2^32 / nk)
     for (int g0 = 0; g0 < b.n_groups; g0 += 65535) {
       const int gy = min(65535, b.n_groups - g0);
       if (b.cpl == 1)
-        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
+        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
       else if (b.cpl == 2)
-        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
+        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
       else
-        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0);
+        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
     }
   }
   HAPT_LAUNCHED("dp_relax");

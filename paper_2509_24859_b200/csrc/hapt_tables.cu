@@ -477,8 +477,8 @@ extern "C" int hapt_tables_init(hapt_tables *t, void *buf, size_t buf_bytes, int
     set_error("hapt_tables_init: invalid dimensions");
     return HAPT_EINVAL;
   }
-  if (L > 65534) {
-    set_error("hapt_tables_init: L=%d exceeds the 16-bit span index", L);
+  if (L >= 4095) {  // 16-bit span index; the DP's multiply-high cell decode needs L < 2^12
+    set_error("hapt_tables_init: L=%d exceeds the supported 4094 layers", L);
     return HAPT_EINVAL;
   }
   Layout y = layout(L, G, n_opts, n_meshes);

@@ -82,6 +82,9 @@ struct Batch {
   uint8_t *kc;         // [n_groups][2*n_meshes][L+1][cw] ceil(2c/t_max)+1 of every
                        // boundary row entry, 0xFF where c > t_max (_dp.pyx:76-82)
   int cb_rows;         // 2*n_meshes
+  int2 *irange[3];     // [n_groups][G+1] (min, max) split i whose successor entry
+                       // (state g) is finite for some candidate of the group;
+                       // layer s reads [(s-1)%3], writes [s%3], resets [(s+1)%3]
   double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
   double *ftop;
@@ -90,7 +93,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, H0, H1, K0, K1, total;
+  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], H0, H1, K0, K1, total;
 };
 
 WsLayout ws_layout(const hapt_tables *t, int n_cand) {
@@ -104,6 +107,10 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   w.tcnt = cur; cur += align_up(np * 4);
   w.cut_sr = cur; cur += align_up(ng * rows * 2);
   w.kc = cur; cur += align_up(ng * 2 * t->n_meshes * (t->L + 1) * cw);
+  for (int j = 0; j < 3; ++j) {
+    w.ir[j] = cur;
+    cur += align_up(ng * (t->G + 1) * sizeof(int2));
+  }
   w.H0 = cur; cur += align_up(ng * hg * cw * 8);
   w.H1 = cur; cur += align_up(ng * hg * cw * 8);
   w.K0 = cur; cur += align_up(ng * hg * cw * 2);
@@ -135,6 +142,14 @@ __global__ void dp_prep(Batch b) {
   for (size_t x = threadIdx.x; x < b.hg * cw; x += blockDim.x) {
     H[x] = kInf;
     K[x] = 0;
+  }
+  // finite-successor ranges: layer 0 has only (g2 = 0, i = L); the buffers
+  // layers 1 and 2 write start empty
+  for (int g = threadIdx.x; g <= b.G; g += blockDim.x) {
+    const int2 empty = make_int2(0x7fffffff, -1);
+    b.irange[0][(size_t)group * (b.G + 1) + g] = g == 0 ? make_int2(b.L, b.L) : empty;
+    b.irange[1][(size_t)group * (b.G + 1) + g] = empty;
+    b.irange[2][(size_t)group * (b.G + 1) + g] = empty;
   }
   if (threadIdx.x < cw) {
     const int cand = group * cw + threadIdx.x;
@@ -314,11 +329,20 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
         const int devs = b.opt_devs[o], g2 = g - devs;
         if (devs <= b.g_avail[g] && g2 >= s - 1) {
           const int row = o * (L + 2) + k;
-          beg = b.span_off[row];
-          // entries with i <= L-s+1 (later successors are provably infinite)
-          // and before the group's suffix-rank cut
-          len = min((int)b.row_pos[(size_t)row * (L + 2) + imax],
-                    (int)b.cut_sr[(size_t)group * b.rows + row]);
+          // admissible splits: i <= L-s+1 (later successors are provably
+          // infinite), inside the range where state g2's successor entry is
+          // finite for some candidate of the group, and before the group's
+          // suffix-rank cut -- every skipped entry is one the reference
+          // skips for all these candidates (fc == inf or tt > t_max)
+          const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
+          const int lo_i = max(k, fr.x), hi_i = min(imax, fr.y);
+          if (lo_i <= hi_i) {
+            const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
+            const int a = pos[lo_i - 1];
+            const int z = min((int)pos[hi_i], (int)b.cut_sr[(size_t)group * b.rows + row]);
+            beg = b.span_off[row] + a;
+            len = max(0, z - a);
+          }
           hbase = g2 * (L + 1);
           // KK <= 3s at layer s: ceil(2c/t_max) <= 2 and N grows by <= 3 per
           // stage, so a row whose thresholds are all >= 3s cannot fail the
@@ -407,11 +431,22 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
       }
     }
     const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
+    bool anyfin = false;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       b.H[s & 1][o_idx + c] = hn[c];
       b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
+      anyfin |= hn[c] != kInf;
     }
+    if (__any_sync(0xffffffffu, anyfin) && lane == 0) {
+      int2 *fr = &b.irange[s % 3][(size_t)group * (G + 1) + g];
+      atomicMin(&fr->x, k - 1);
+      atomicMax(&fr->y, k - 1);
+    }
+  }
+  if (blockIdx.x == 0) {  // the buffer layer s+1 writes: last read by layer s-1
+    for (int x = threadIdx.x; x <= G; x += blockDim.x)
+      b.irange[(s + 1) % 3][(size_t)group * (G + 1) + x] = make_int2(0x7fffffff, -1);
   }
 #pragma unroll
   for (int c = 0; c < CPL; ++c) fin_cnt[warp][lane * CPL + c] = fin[c];
@@ -613,6 +648,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.cut_sr = (uint16_t *)(wb + w.cut_sr);
   b.kc = (uint8_t *)(wb + w.kc);
   b.cb_rows = 2 * t->n_meshes;
+  for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);
   b.H[0] = (double *)(wb + w.H0);
   b.H[1] = (double *)(wb + w.H1);
   b.K[0] = (uint16_t *)(wb + w.K0);

@@ -367,6 +367,16 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bytes_per_launch / avg_launch_s / 1e9
     fp64 = fp64_peak(lib, torch, device)
+    # measured DRAM bytes per dp_relax launch of this workload, from the ncu
+    # metrics pass committed under profiles/ (tools/ncu_traffic.py)
+    traffic = None
+    try:
+        with open(os.path.join(REPO, "profiles", "dp_relax_traffic.json")) as fh:
+            tr = json.load(fh)
+        if tr.get("config") == args.config:
+            traffic = tr["dram_bytes_per_launch"] * n_mine / tr["pool_candidates"]
+    except (OSError, KeyError, ValueError):
+        pass
     roofline = {
         "bound": "hbm",
         "kernel": "dp_relax (hapt_dp.cu)",
@@ -374,7 +384,8 @@ def main():
         "peak": hbm_peak,
         "unit": "GB/s",
         "frac": achieved / hbm_peak,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write, mean over a sweep)",
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
         "algorithmic_bytes_per_candidate": bytes_per_cand,
         "fp64": {
@@ -474,7 +485,7 @@ def per_config(args, torch, device) -> dict:
     from paper_2509_24859_b200.workloads import config_e, instance
 
     out = {}
-    for name in ("A", "B", "C", "D1"):
+    for name in ("A", "B", "C", "D1", "D2", "D3"):
         layers, cluster, model, rho, B, eps = instance(name)
         st = build_store(layers, cluster, model, imbalance_ratio=rho)
         costs = boundary_costs(layers, cluster)
@@ -486,13 +497,17 @@ def per_config(args, torch, device) -> dict:
             st2 = build_store(layers, cluster, model, imbalance_ratio=rho)
             plan = search(st2, boundary_costs(layers, cluster), B, epsilon=eps)
             ts.append(time.perf_counter() - t0)
+        out[name] = {"search_time_s": min(ts), "plan_stages": plan.num_stages,
+                     "T*": plan.predicted_latency, "t_max": plan.t_max,
+                     "evaluated": plan.search_stats["evaluated"],
+                     "pool": plan.search_stats["candidates_total"]}
+        if name in ("D2", "D3"):
+            continue  # full pools of 7k / 16k candidates: search only in the default run
+        sweep_pool(st, costs, B)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pool, tstar, bs, states, w = sweep_pool(st, costs, B)
-        dt = time.perf_counter() - t0
-        out[name] = {"search_time_s": min(ts), "full_pool_candidates_per_s": len(pool) / dt,
-                     "pool": len(pool), "plan_stages": plan.num_stages,
-                     "T*": plan.predicted_latency}
+        out[name]["full_pool_candidates_per_s"] = len(pool) / (time.perf_counter() - t0)
     n = 1_000_000
     f, b, c, S = config_e(n)
     F, Bt, C, Sd = (torch.from_numpy(x).to(device) for x in (f, b, c, S))

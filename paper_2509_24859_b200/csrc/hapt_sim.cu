@@ -106,13 +106,16 @@ __device__ __forceinline__ int decode_op(int pos, int N, int B, bool &isF) {
   return steady + (q - 2 * steady) + 1;
 }
 
-__global__ void k_sim(int n_plans, const int32_t *stage_off, const double *t_fwd,
+__global__ void k_sim(int n_plans, const int32_t *perm, const int32_t *n_perm,
+                      const int32_t *stage_off, const double *t_fwd,
                       const double *t_bwd, const double *comm, const int32_t *counts,
                       const int32_t *num_mb, double *makespan, double *node_start,
                       double *node_end, const int64_t *node_off, int R, double *ring,
                       int32_t *status) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_plans) return;
+  // all plans (perm == NULL) or the n_perm[0] plans listed in perm
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (perm ? *n_perm : n_plans)) return;
+  const int p = perm ? perm[t] : t;
   const int b0 = stage_off[p], S = stage_off[p + 1] - b0, B = num_mb[p];
   if (S < 1 || S > kMaxStages || B < 1) {
     status[p] = HAPT_ESCHED;
@@ -287,6 +290,168 @@ __global__ void k_dag(int n, const int32_t *succ_off, const int32_t *succ_idx,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path for plans with S <= 8 stages (config E): S is a template
+// parameter, so every per-stage recurrence value (program position, last end
+// on the stage, last transfer end per link direction, ops done) lives in
+// registers; the per-link transfer FIFOs live in shared memory, [slot][thread]
+// so a warp's accesses are conflict-free.  Stages advance round-robin, one op
+// per sweep, which keeps the FIFOs shallow; a producer whose FIFO is full
+// waits (max-plus results do not depend on the processing order).  A plan
+// that stops progressing (a program that deadlocks, or FIFO capacity
+// exceeded by unusual counts) is marked for the generic kernel.
+// ---------------------------------------------------------------------------
+constexpr int kRing = 8;
+constexpr int kRetry = -1;
+
+template <int S>
+struct SimCfg {
+  static constexpr int threads = S >= 6 ? 64 : 128;
+  static constexpr size_t smem = (size_t)(S > 1 ? S - 1 : 1) * 2 * kRing * threads * 8;
+};
+
+template <int S>
+__global__ void __launch_bounds__(SimCfg<S>::threads)
+    k_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
+            const double *t_bwd, const double *comm, const int32_t *counts,
+            const int32_t *num_mb, double *makespan, int32_t *status) {
+  extern __shared__ double ring[];  // [(S-1) links][2 dirs][kRing][threads]
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int p = perm[t];
+  const int b0 = stage_off[p], B = num_mb[p];
+  int N[S];
+  double tf[S], tb[S], cm[S > 1 ? S - 1 : 1];
+  bool bad = B < 1;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    N[s] = counts[b0 + s];
+    tf[s] = t_fwd[b0 + s];
+    tb[s] = t_bwd[b0 + s];
+    if (s + 1 < S) cm[s] = comm[b0 + s];
+    bad |= N[s] < 1 || N[s] > B;
+  }
+  // build_program preconditions (scheduling.py:235-239, 61-66)
+  if (bad || N[S - 1] != 1) {
+    status[p] = HAPT_ESCHED;
+    return;
+  }
+  const int ld = blockDim.x;
+  auto slot = [&](int link, int dir, int mb) -> double & {
+    return ring[(((link * 2 + dir) * kRing + (mb & (kRing - 1))) * ld) + threadIdx.x];
+  };
+  int pos[S], fd[S], bd[S];
+  double prev[S], lcf[S], lcb[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    pos[s] = fd[s] = bd[s] = 0;
+    prev[s] = lcf[s] = lcb[s] = 0.0;
+  }
+  double mk = 0.0;
+  int remaining = S;
+  while (remaining > 0) {
+    bool progress = false;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      if (pos[s] < 2 * B) {
+        bool isF;
+        const int mb = decode_op(pos[s], N[s], B, isF);
+        bool ready;
+        if (isF)
+          ready = (s == 0 || fd[s - 1] >= mb) && (s == S - 1 || mb - fd[s + 1] <= kRing);
+        else
+          ready = (s == S - 1 || bd[s + 1] >= mb) && (s == 0 || mb - bd[s - 1] <= kRing);
+        if (ready) {
+          double dep = 0.0;
+          if (isF && s > 0) dep = slot(s - 1, 0, mb);
+          if (!isF && s < S - 1) dep = slot(s, 1, mb);
+          const double st = fmax(prev[s], dep);
+          const double en = __dadd_rn(st, isF ? tf[s] : tb[s]);
+          prev[s] = en;
+          mk = fmax(mk, en);
+          if (isF) {
+            fd[s] = mb;
+            if (s < S - 1) {  // forward transfer on link s (simulation.py:130-140)
+              const double ce = __dadd_rn(fmax(en, lcf[s]), cm[s]);
+              lcf[s] = ce;
+              mk = fmax(mk, ce);
+              slot(s, 0, mb) = ce;
+            }
+          } else {
+            bd[s] = mb;
+            if (s > 0) {  // backward transfer on link s-1
+              const double ce = __dadd_rn(fmax(en, lcb[s - 1]), cm[s - 1]);
+              lcb[s - 1] = ce;
+              mk = fmax(mk, ce);
+              slot(s - 1, 1, mb) = ce;
+            }
+          }
+          if (++pos[s] == 2 * B) --remaining;
+          progress = true;
+        }
+      }
+    }
+    if (!progress) {
+      status[p] = kRetry;  // let the generic kernel decide (deadlock vs. depth)
+      return;
+    }
+  }
+  makespan[p] = mk;
+  status[p] = HAPT_OK;
+}
+
+__global__ void k_sim_bucket(int n_plans, const int32_t *stage_off, int32_t *cnt /*[10]*/,
+                             int32_t *perm) {
+  // two-phase counting sort of plan indices by stage count (1..8, else 0),
+  // stable within a bucket; run with a single block
+  __shared__ int c[9], base[9];
+  if (threadIdx.x < 9) c[threadIdx.x] = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < n_plans; p += blockDim.x) {
+    const int S = stage_off[p + 1] - stage_off[p];
+    atomicAdd(&c[(S >= 1 && S <= 8) ? S : 0], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int b = 0; b < 9; ++b) {
+      base[b] = run;
+      cnt[b] = c[b];
+      run += c[b];
+      c[b] = 0;
+    }
+    cnt[9] = run;
+  }
+  __syncthreads();
+  // deterministic order is not required for correctness (plans are
+  // independent); atomics give each plan a slot in its bucket
+  for (int p = threadIdx.x; p < n_plans; p += blockDim.x) {
+    const int S = stage_off[p + 1] - stage_off[p];
+    const int b = (S >= 1 && S <= 8) ? S : 0;
+    perm[base[b] + atomicAdd(&c[b], 1)] = p;
+  }
+}
+
+__global__ void k_sim_retry(int n_plans, const int32_t *status, int32_t *perm, int32_t *n_out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n_plans && status[p] == kRetry) perm[atomicAdd(n_out, 1)] = p;
+}
+
+template <int S>
+void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
+                  const double *t_bwd, const double *comm, const int32_t *counts,
+                  const int32_t *num_mb, double *makespan, int32_t *status, cudaStream_t st) {
+  if (n <= 0) return;
+  using C = SimCfg<S>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sim_s<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+    attr = true;
+  }
+  k_sim_s<S><<<grid_for(n, C::threads), C::threads, C::smem, st>>>(
+      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status);
+}
+
 }  // namespace
 }  // namespace hapt
 
@@ -308,7 +473,9 @@ extern "C" int hapt_launch_counts(int32_t n_plans, const int32_t *stage_off, con
 }
 
 extern "C" size_t hapt_sim_workspace_bytes(int64_t total_stages, int32_t ring_depth) {
-  return align_up((size_t)(total_stages > 0 ? total_stages : 1) * 2 * ring_depth * 8);
+  const size_t ts = (size_t)(total_stages > 0 ? total_stages : 1);
+  // generic-kernel FIFOs + plan permutation (n_plans <= total_stages) + counters
+  return align_up(ts * 2 * ring_depth * 8) + align_up(ts * 4) + align_up(16 * 4);
 }
 
 extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
@@ -322,10 +489,53 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
     set_error("hapt_sim_1f1b: invalid arguments");
     return HAPT_EINVAL;
   }
-  (void)work_bytes;
-  k_sim<<<grid_for(n_plans, 128), 128, 0, (cudaStream_t)stream>>>(
-      n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, node_start, node_end,
-      node_off, ring_depth, (double *)work, status);
+  cudaStream_t st = (cudaStream_t)stream;
+  // total stages = stage_off[n_plans] lives on the device; the caller sized
+  // `work` with hapt_sim_workspace_bytes(total_stages, ring_depth), so the
+  // ring region is what remains after the permutation and counters
+  const size_t tail = align_up((size_t)n_plans * 4) + align_up(16 * 4);
+  if (work_bytes < tail + 2 * (size_t)ring_depth * 8) {
+    set_error("hapt_sim_1f1b: workspace too small");
+    return HAPT_ENOSPACE;
+  }
+  double *ring = (double *)work;
+  char *wt = (char *)work + (work_bytes - tail);
+  int32_t *perm = (int32_t *)wt;
+  int32_t *cnt = (int32_t *)(wt + align_up((size_t)n_plans * 4));
+  if (node_start) {  // per-node outputs (simulate() on one plan): generic walk
+    k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, nullptr, nullptr, stage_off, t_fwd,
+                                                  t_bwd, comm, counts, num_mb, makespan,
+                                                  node_start, node_end, node_off, ring_depth,
+                                                  ring, status);
+    HAPT_LAUNCHED("k_sim");
+    return HAPT_OK;
+  }
+  k_sim_bucket<<<1, 1024, 0, st>>>(n_plans, stage_off, cnt, perm);
+  int32_t h[10];
+  HAPT_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+  HAPT_CUDA(cudaStreamSynchronize(st));
+  int off = h[0];  // bucket 0 (S > 8): generic kernel below
+#define HAPT_SIM_S(SV)                                                                    \
+  launch_sim_s<SV>(perm + off, h[SV], stage_off, t_fwd, t_bwd, comm, counts, num_mb,      \
+                   makespan, status, st);                                                 \
+  off += h[SV];
+  HAPT_SIM_S(1) HAPT_SIM_S(2) HAPT_SIM_S(3) HAPT_SIM_S(4)
+  HAPT_SIM_S(5) HAPT_SIM_S(6) HAPT_SIM_S(7) HAPT_SIM_S(8)
+#undef HAPT_SIM_S
+  HAPT_LAUNCHED("k_sim_s");
+  // plans with S > 8 (bucket 0, first h[0] entries of perm) plus any plan the
+  // fast path handed back: gather them into perm[0..) and run the generic walk
+  HAPT_CUDA(cudaMemsetAsync(cnt + 12, 0, 4, st));
+  k_sim_retry<<<grid_for(n_plans, 256), 256, 0, st>>>(n_plans, status, perm + h[0], cnt + 12);
+  // bucket 0 occupies perm[0..h[0]); retries were appended after it at
+  // perm[h[0]..); run the generic kernel over both ranges
+  k_sim<<<grid_for(h[0], 128), 128, 0, st>>>(h[0], perm, cnt + 0, stage_off, t_fwd, t_bwd,
+                                             comm, counts, num_mb, makespan, nullptr, nullptr,
+                                             nullptr, ring_depth, ring, status);
+  k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, perm + h[0], cnt + 12, stage_off,
+                                                t_fwd, t_bwd, comm, counts, num_mb, makespan,
+                                                nullptr, nullptr, nullptr, ring_depth, ring,
+                                                status);
   HAPT_LAUNCHED("k_sim");
   return HAPT_OK;
 }

@@ -301,7 +301,10 @@ __global__ void k_dag(int n, const int32_t *succ_off, const int32_t *succ_idx,
 // that stops progressing (a program that deadlocks, or FIFO capacity
 // exceeded by unusual counts) is marked for the generic kernel.
 // ---------------------------------------------------------------------------
-constexpr int kRing = 8;
+#ifndef HAPT_SIM_RING
+#define HAPT_SIM_RING 4
+#endif
+constexpr int kRing = HAPT_SIM_RING;  // FIFO slots per link direction (power of two)
 constexpr int kRetry = -1;
 
 template <int S>
@@ -400,35 +403,57 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
   status[p] = HAPT_OK;
 }
 
-__global__ void k_sim_bucket(int n_plans, const int32_t *stage_off, int32_t *cnt /*[10]*/,
-                             int32_t *perm) {
-  // two-phase counting sort of plan indices by stage count (1..8, else 0),
-  // stable within a bucket; run with a single block
-  __shared__ int c[9], base[9];
+// Counting sort of plan indices by stage count (bucket S for 1..8, bucket 0
+// for S > 8): per-block histograms, one scan, per-block scatter.  Order inside
+// a bucket is irrelevant (plans are independent).
+constexpr int kBucketBlock = 1024;
+
+__device__ __forceinline__ int bucket_of(const int32_t *stage_off, int p) {
+  const int S = stage_off[p + 1] - stage_off[p];
+  return (S >= 1 && S <= 8) ? S : 0;
+}
+
+__global__ void k_bucket_hist(int n_plans, const int32_t *stage_off, int32_t *bhist) {
+  __shared__ int c[9];
   if (threadIdx.x < 9) c[threadIdx.x] = 0;
   __syncthreads();
-  for (int p = threadIdx.x; p < n_plans; p += blockDim.x) {
-    const int S = stage_off[p + 1] - stage_off[p];
-    atomicAdd(&c[(S >= 1 && S <= 8) ? S : 0], 1);
-  }
+  const int p = blockIdx.x * kBucketBlock + threadIdx.x;
+  if (p < n_plans) atomicAdd(&c[bucket_of(stage_off, p)], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 9) bhist[blockIdx.x * 9 + threadIdx.x] = c[threadIdx.x];
+}
+
+__global__ void k_bucket_scan(int n_blocks, int32_t *bhist, int32_t *cnt) {
+  // one thread per bucket: exclusive scan over blocks, then bucket bases
+  __shared__ int tot[9];
+  const int b = threadIdx.x;
+  if (b < 9) {
     int run = 0;
-    for (int b = 0; b < 9; ++b) {
-      base[b] = run;
-      cnt[b] = c[b];
-      run += c[b];
-      c[b] = 0;
+    for (int k = 0; k < n_blocks; ++k) {
+      const int v = bhist[k * 9 + b];
+      bhist[k * 9 + b] = run;
+      run += v;
     }
-    cnt[9] = run;
+    tot[b] = run;
+    cnt[b] = run;
   }
   __syncthreads();
-  // deterministic order is not required for correctness (plans are
-  // independent); atomics give each plan a slot in its bucket
-  for (int p = threadIdx.x; p < n_plans; p += blockDim.x) {
-    const int S = stage_off[p + 1] - stage_off[p];
-    const int b = (S >= 1 && S <= 8) ? S : 0;
-    perm[base[b] + atomicAdd(&c[b], 1)] = p;
+  if (b < 9) {
+    int base = 0;
+    for (int q = 0; q < b; ++q) base += tot[q];
+    cnt[10 + b] = base;  // bucket start in perm
+  }
+}
+
+__global__ void k_bucket_scatter(int n_plans, const int32_t *stage_off, const int32_t *bhist,
+                                 const int32_t *cnt, int32_t *perm) {
+  __shared__ int c[9];
+  if (threadIdx.x < 9) c[threadIdx.x] = 0;
+  __syncthreads();
+  const int p = blockIdx.x * kBucketBlock + threadIdx.x;
+  if (p < n_plans) {
+    const int b = bucket_of(stage_off, p);
+    perm[cnt[10 + b] + bhist[blockIdx.x * 9 + b] + atomicAdd(&c[b], 1)] = p;
   }
 }
 
@@ -472,10 +497,18 @@ extern "C" int hapt_launch_counts(int32_t n_plans, const int32_t *stage_off, con
   return HAPT_OK;
 }
 
+namespace {
+// tail of the workspace: plan permutation, bucket counters, block histograms
+size_t sim_tail_bytes(size_t n_plans) {
+  return align_up(n_plans * 4) + align_up(32 * 4) +
+         align_up((n_plans / kBucketBlock + 1) * 9 * 4);
+}
+}  // namespace
+
 extern "C" size_t hapt_sim_workspace_bytes(int64_t total_stages, int32_t ring_depth) {
   const size_t ts = (size_t)(total_stages > 0 ? total_stages : 1);
-  // generic-kernel FIFOs + plan permutation (n_plans <= total_stages) + counters
-  return align_up(ts * 2 * ring_depth * 8) + align_up(ts * 4) + align_up(16 * 4);
+  // generic-kernel FIFOs + tail sized for n_plans <= total_stages
+  return align_up(ts * 2 * ring_depth * 8) + sim_tail_bytes(ts);
 }
 
 extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
@@ -492,8 +525,8 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   cudaStream_t st = (cudaStream_t)stream;
   // total stages = stage_off[n_plans] lives on the device; the caller sized
   // `work` with hapt_sim_workspace_bytes(total_stages, ring_depth), so the
-  // ring region is what remains after the permutation and counters
-  const size_t tail = align_up((size_t)n_plans * 4) + align_up(16 * 4);
+  // ring region is what remains after the tail
+  const size_t tail = sim_tail_bytes((size_t)n_plans);
   if (work_bytes < tail + 2 * (size_t)ring_depth * 8) {
     set_error("hapt_sim_1f1b: workspace too small");
     return HAPT_ENOSPACE;
@@ -502,6 +535,7 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   char *wt = (char *)work + (work_bytes - tail);
   int32_t *perm = (int32_t *)wt;
   int32_t *cnt = (int32_t *)(wt + align_up((size_t)n_plans * 4));
+  int32_t *bhist = cnt + 32;
   if (node_start) {  // per-node outputs (simulate() on one plan): generic walk
     k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, nullptr, nullptr, stage_off, t_fwd,
                                                   t_bwd, comm, counts, num_mb, makespan,
@@ -510,29 +544,50 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
     HAPT_LAUNCHED("k_sim");
     return HAPT_OK;
   }
-  k_sim_bucket<<<1, 1024, 0, st>>>(n_plans, stage_off, cnt, perm);
-  int32_t h[10];
+  const int nb = (n_plans + kBucketBlock - 1) / kBucketBlock;
+  k_bucket_hist<<<nb, kBucketBlock, 0, st>>>(n_plans, stage_off, bhist);
+  k_bucket_scan<<<1, 32, 0, st>>>(nb, bhist, cnt);
+  k_bucket_scatter<<<nb, kBucketBlock, 0, st>>>(n_plans, stage_off, bhist, cnt, perm);
+  int32_t h[19];  // [0..8] bucket sizes, [10..18] bucket starts in perm
   HAPT_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
   HAPT_CUDA(cudaStreamSynchronize(st));
-  int off = h[0];  // bucket 0 (S > 8): generic kernel below
-#define HAPT_SIM_S(SV)                                                                    \
-  launch_sim_s<SV>(perm + off, h[SV], stage_off, t_fwd, t_bwd, comm, counts, num_mb,      \
-                   makespan, status, st);                                                 \
-  off += h[SV];
-  HAPT_SIM_S(1) HAPT_SIM_S(2) HAPT_SIM_S(3) HAPT_SIM_S(4)
-  HAPT_SIM_S(5) HAPT_SIM_S(6) HAPT_SIM_S(7) HAPT_SIM_S(8)
+  HAPT_LAUNCHED("k_bucket");
+  // the eight per-S kernels are independent: run them concurrently on side
+  // streams (each alone occupies the GPU only partially), joined back to st
+  static thread_local cudaStream_t side[9];
+  static thread_local cudaEvent_t ev[10];
+  static thread_local bool init = false;
+  if (!init) {
+    for (int q = 1; q <= 8; ++q) {
+      HAPT_CUDA(cudaStreamCreateWithFlags(&side[q], cudaStreamNonBlocking));
+      HAPT_CUDA(cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming));
+    }
+    HAPT_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    init = true;
+  }
+  HAPT_CUDA(cudaEventRecord(ev[0], st));
+  // bucket 0 (S > 8) goes through the generic kernel below
+#define HAPT_SIM_S(SV)                                                                        \
+  if (h[SV] > 0) {                                                                            \
+    HAPT_CUDA(cudaStreamWaitEvent(side[SV], ev[0], 0));                                       \
+    launch_sim_s<SV>(perm + h[10 + SV], h[SV], stage_off, t_fwd, t_bwd, comm, counts, num_mb, \
+                     makespan, status, side[SV]);                                             \
+    HAPT_CUDA(cudaEventRecord(ev[SV], side[SV]));                                             \
+    HAPT_CUDA(cudaStreamWaitEvent(st, ev[SV], 0));                                            \
+  }
+  HAPT_SIM_S(8) HAPT_SIM_S(7) HAPT_SIM_S(6) HAPT_SIM_S(5)
+  HAPT_SIM_S(4) HAPT_SIM_S(3) HAPT_SIM_S(2) HAPT_SIM_S(1)
 #undef HAPT_SIM_S
   HAPT_LAUNCHED("k_sim_s");
-  // plans with S > 8 (bucket 0, first h[0] entries of perm) plus any plan the
-  // fast path handed back: gather them into perm[0..) and run the generic walk
-  HAPT_CUDA(cudaMemsetAsync(cnt + 12, 0, 4, st));
-  k_sim_retry<<<grid_for(n_plans, 256), 256, 0, st>>>(n_plans, status, perm + h[0], cnt + 12);
-  // bucket 0 occupies perm[0..h[0]); retries were appended after it at
-  // perm[h[0]..); run the generic kernel over both ranges
-  k_sim<<<grid_for(h[0], 128), 128, 0, st>>>(h[0], perm, cnt + 0, stage_off, t_fwd, t_bwd,
-                                             comm, counts, num_mb, makespan, nullptr, nullptr,
-                                             nullptr, ring_depth, ring, status);
-  k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, perm + h[0], cnt + 12, stage_off,
+  // plans with S > 8 (bucket 0 = perm[0..h[0])) and any plan the fast path
+  // handed back (appended after bucket 0) go through the generic walk
+  HAPT_CUDA(cudaMemsetAsync(cnt + 20, 0, 4, st));
+  if (h[0] > 0)
+    k_sim<<<grid_for(h[0], 128), 128, 0, st>>>(h[0], perm, cnt + 0, stage_off, t_fwd, t_bwd,
+                                               comm, counts, num_mb, makespan, nullptr, nullptr,
+                                               nullptr, ring_depth, ring, status);
+  k_sim_retry<<<grid_for(n_plans, 256), 256, 0, st>>>(n_plans, status, perm + h[0], cnt + 20);
+  k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, perm + h[0], cnt + 20, stage_off,
                                                 t_fwd, t_bwd, comm, counts, num_mb, makespan,
                                                 nullptr, nullptr, nullptr, ring_depth, ring,
                                                 status);

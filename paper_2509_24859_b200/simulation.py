@@ -336,6 +336,90 @@ def _sim_call(t_fwd, t_bwd, comm, counts, num_mb, want_nodes=False, stage_counts
     return mk, status
 
 
+class PlanBatch:
+    """Many plans packed once on the device (plan p owns stages
+    [stage_off[p], stage_off[p+1]); comm[stage_off[p] + j] is boundary j).
+    Built from dense [P, S] arrays (+ optional per-plan stage counts)."""
+
+    def __init__(self, t_fwd, t_bwd, comm, stage_counts=None, device=None):
+        import torch
+
+        dev = device or (t_fwd.device if isinstance(t_fwd, torch.Tensor) and t_fwd.is_cuda
+                         else torch.device("cuda", torch.cuda.current_device()))
+        T = lambda a, dt=torch.float64: torch.as_tensor(a, dtype=dt).to(dev).contiguous()  # noqa: E731
+        tf, tb, cm = T(t_fwd), T(t_bwd), T(comm)
+        P, S = tf.shape
+        self.n_plans, self.width, self.device = P, S, dev
+        if stage_counts is None:
+            self.stage_off = torch.arange(0, (P + 1) * S, S, dtype=torch.int32, device=dev)
+            self.t_fwd, self.t_bwd, self.comm = tf.reshape(-1), tb.reshape(-1), cm.reshape(-1)
+            self.max_stages = S
+        else:
+            sc = T(stage_counts, torch.int32)
+            self.stage_off = torch.zeros(P + 1, dtype=torch.int32, device=dev)
+            self.stage_off[1:] = torch.cumsum(sc, 0)
+            mask = torch.arange(S, device=dev)[None, :] < sc[:, None].long()
+            self.t_fwd, self.t_bwd, self.comm = (x[mask].contiguous() for x in (tf, tb, cm))
+            self.max_stages = int(sc.max().item())
+        self.total_stages = int(self.t_fwd.numel())
+
+    def counts(self, epsilon: float = 0.05, kind: str = "adaptive", tmax=None):
+        """Packed launch counts (hapt_launch_counts) and per-plan status."""
+        import torch
+
+        from . import _lib
+        from ._lib import check, stream_ptr
+
+        counts = torch.empty(self.total_stages, dtype=torch.int32, device=self.device)
+        status = torch.empty(self.n_plans, dtype=torch.int32, device=self.device)
+        kind_id = {"classic": _lib.COUNTS_CLASSIC, "eager": _lib.COUNTS_EAGER,
+                   "adaptive": _lib.COUNTS_ADAPTIVE}[kind]
+        tm = None if tmax is None else torch.as_tensor(tmax, dtype=torch.float64).to(self.device)
+        check(_lib.lib().hapt_launch_counts(
+            self.n_plans, self.stage_off.data_ptr(), self.t_fwd.data_ptr(),
+            self.t_bwd.data_ptr(), self.comm.data_ptr(), 0 if tm is None else tm.data_ptr(),
+            float(epsilon), kind_id, counts.data_ptr(), status.data_ptr(), stream_ptr()))
+        return counts, status
+
+    def simulate(self, counts, num_microbatches, ring_depth: int | None = None):
+        """Makespans (hapt_sim_1f1b) for packed counts; returns (makespan,
+        status) CUDA tensors."""
+        import torch
+
+        from . import _lib
+        from ._lib import check, stream_ptr
+
+        lib = _lib.lib()
+        mb = torch.as_tensor(num_microbatches, dtype=torch.int32).to(self.device).reshape(-1)
+        if mb.numel() == 1 and self.n_plans > 1:
+            mb = mb.expand(self.n_plans).contiguous()
+        if ring_depth is None:  # generic-kernel FIFO depth >= N_1 + 1
+            ring_depth = int(counts.max().item()) + 2
+        nb = lib.hapt_sim_workspace_bytes(self.total_stages, ring_depth)
+        ws = _sim_ws(self.device, nb)
+        mk = torch.empty(self.n_plans, dtype=torch.float64, device=self.device)
+        status = torch.empty(self.n_plans, dtype=torch.int32, device=self.device)
+        check(lib.hapt_sim_1f1b(self.n_plans, self.stage_off.data_ptr(), self.t_fwd.data_ptr(),
+                                self.t_bwd.data_ptr(), self.comm.data_ptr(), counts.data_ptr(),
+                                mb.data_ptr(), mk.data_ptr(), 0, 0, 0, ring_depth,
+                                status.data_ptr(), ws.data_ptr(), nb, stream_ptr()))
+        return mk, status
+
+
+_SIM_WS: dict = {}
+
+
+def _sim_ws(device, nbytes):
+    import torch
+
+    buf = _SIM_WS.get(device)
+    if buf is None or buf.numel() < nbytes:
+        _SIM_WS.pop(device, None)
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _SIM_WS[device] = buf
+    return buf
+
+
 def simulate_batch(t_fwd, t_bwd, comm, counts, num_microbatches, stage_counts=None):
     """Makespans of many 1F1B plans in one launch (config E).
 

@@ -21,21 +21,19 @@ def main():
     import numpy as np
     import torch
 
-    from paper_2509_24859_b200.scheduling import launch_counts_batch
-    from paper_2509_24859_b200.simulation import simulate_batch
+    from paper_2509_24859_b200.simulation import PlanBatch
     from paper_2509_24859_b200.workloads import config_e
 
     n = args.plans
     f, b, c, S = config_e(n)
     dev = torch.device("cuda", 0)
-    F, Bt, C, Sd = (torch.from_numpy(x).to(dev) for x in (f, b, c, S))
-    mask = torch.arange(8, device=dev)[None, :] < Sd[:, None].long()
-    dense = torch.zeros((n, 8), dtype=torch.int32, device=dev)
+    batch = PlanBatch(f, b, c, stage_counts=S, device=dev)
+    off = np.concatenate([[0], np.cumsum(S)])
 
     def step():
-        counts, status = launch_counts_batch(F, Bt, C, kind="adaptive", stage_counts=Sd)
-        dense[mask] = counts
-        return simulate_batch(F, Bt, C, dense, 128, stage_counts=Sd)
+        counts, status = batch.counts(0.05, "adaptive")
+        step.counts = counts
+        return batch.simulate(counts, 128, ring_depth=26)
 
     for _ in range(2):
         mk, st = step()
@@ -53,11 +51,13 @@ def main():
         import oracle as O
 
         mkh = mk.cpu().numpy()
-        dh = dense.cpu().numpy()
+        ch = step.counts.cpu().numpy()
         bad = 0
         for p in range(0, n, max(1, n // args.check)):
             s_ = int(S[p])
-            want, _, _ = O.simulate(f[p, :s_], b[p, :s_], c[p, : s_ - 1], list(dh[p, :s_]), 128)
+            cnt = list(ch[off[p]: off[p + 1]])
+            assert cnt == O.adaptive_counts(list(f[p, :s_] + b[p, :s_]), list(c[p, : s_ - 1]), 0.05)
+            want, _, _ = O.simulate(f[p, :s_], b[p, :s_], c[p, : s_ - 1], cnt, 128)
             bad += mkh[p] != want
         print(f"parity: {args.check} sampled plans, {bad} mismatches")
 

@@ -85,6 +85,10 @@ struct Batch {
   int2 *irange[3];     // [n_groups][G+1] (min, max) split i whose successor entry
                        // (state g) is finite for some candidate of the group;
                        // layer s reads [(s-1)%3], writes [s%3], resets [(s+1)%3]
+  uint16_t *maxlen;    // [n_groups][n_opts] longest admissible span of an option
+  short2 *kwin;        // [n_groups][G+1] first/last k whose cell can be finite at
+                       // the current layer (dp_window)
+  int n_opts;
   double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
   double *ftop;
@@ -93,7 +97,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], H0, H1, K0, K1, total;
+  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], maxlen, kwin, H0, H1, K0, K1, total;
 };
 
 WsLayout ws_layout(const hapt_tables *t, int n_cand) {
@@ -111,6 +115,8 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
     w.ir[j] = cur;
     cur += align_up(ng * (t->G + 1) * sizeof(int2));
   }
+  w.maxlen = cur; cur += align_up(ng * t->n_opts * 2);
+  w.kwin = cur; cur += align_up(ng * (t->G + 1) * sizeof(short2));
   w.H0 = cur; cur += align_up(ng * hg * cw * 8);
   w.H1 = cur; cur += align_up(ng * hg * cw * 8);
   w.K0 = cur; cur += align_up(ng * hg * cw * 2);
@@ -172,6 +178,21 @@ __global__ void dp_prep(Batch b) {
     }
     b.cut_sr[(size_t)group * b.rows + row] = (uint16_t)(lo - beg);
   }
+  __syncthreads();
+  // longest admissible span (before the cut) of each option, for dp_window
+  for (int o = threadIdx.x; o < b.n_opts; o += blockDim.x) {
+    int ml = 0;
+    for (int k = 1; k <= b.L; ++k) {
+      const int row = o * (b.L + 2) + k;
+      const int cut = b.cut_sr[(size_t)group * b.rows + row];
+      if (cut > 0) {
+        // entries are in ascending span end: the last admissible one is the longest
+        const int beg = b.span_off[row];
+        ml = max(ml, (int)b.spans[beg + cut - 1].i - k + 1);
+      }
+    }
+    b.maxlen[(size_t)group * b.n_opts + o] = (uint16_t)ml;
+  }
   // the launch-bound increment of every boundary entry for every candidate:
   // kk = (ceil(2c/t_max) + 1) + N (_dp.pyx:82, same association); c > t_max
   // skips the transition (_dp.pyx:76-78) -> 0xFF
@@ -193,6 +214,36 @@ __global__ void dp_prep(Batch b) {
       H[e] = __dadd_rn(c2, 0.0);
       K[e] = (uint16_t)((int)ceil(__ddiv_rn(c2, tm)) + 1);
     }
+  }
+}
+
+// Per (group, state g) at layer s: the hull of k whose cell (k, g) can have an
+// admissible transition -- through option o only splits i in the previous
+// layer's finite range [lo, hi] of g2 = g - devs, i <= L-s+1, and spans no
+// longer than the option's longest admissible one qualify, so
+// k in [lo - maxlen_o + 1, min(hi, L-s+1)].  Cells outside the hull are
+// provably infinite and are never read by layer s+1 (its read range comes
+// from cells that were finite), so dp_relax skips them without writing.
+__global__ void dp_window(Batch b, int s) {
+  const int group = blockIdx.x;
+  const int L = b.L, G = b.G, imax = L - s + 1;
+  for (int g = threadIdx.x; g <= G; g += blockDim.x) {
+    int klo = 0x7fff, khi = 0;
+    if (g >= s) {
+      const int r = b.g_mesh[g], avail = b.g_avail[g];
+      for (int o = b.opt_off[r]; o < b.opt_off[r + 1]; ++o) {
+        const int devs = b.opt_devs[o], g2 = g - devs;
+        if (devs > avail || g2 < s - 1) continue;
+        const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
+        const int hi = min(imax, fr.y);
+        if (fr.x > hi) continue;
+        const int ml = b.maxlen[(size_t)group * b.n_opts + o];
+        if (ml == 0) continue;
+        klo = min(klo, max(1, fr.x - ml + 1));
+        khi = max(khi, hi);
+      }
+    }
+    b.kwin[(size_t)group * (G + 1) + g] = make_short2((short)klo, (short)khi);
   }
 }
 
@@ -273,7 +324,7 @@ __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
 
 template <int CPL>
 __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
-    dp_relax(Batch b, int s, int group0, unsigned long long nk_magic) {
+    dp_relax(Batch b, int s, int group0, unsigned long long nk_magic, int use_window) {
   constexpr int CW = 32 * CPL;
   __shared__ int fin_cnt[kWarps][CW];
   __shared__ int4 stage_e[kWarps][32];
@@ -283,17 +334,21 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   const int L = b.L, G = b.G;
   const int nk = L - s + 1, ng = G - s + 1;
   const int cell = blockIdx.x * kWarps + warp;
-  const bool active = cell < nk * ng;
+  // cell / nk by multiply-high with ceil(2^32/nk): exact for cell < 2^20,
+  // nk < 2^12 (hapt_tables_init bounds both)
+  const int gq = (int)(((unsigned long long)(unsigned)cell * nk_magic) >> 32);
+  const int k = 1 + cell - gq * nk;
+  const int g = s + gq;
+  bool active = cell < nk * ng;
+  if (active && use_window) {  // outside the window: provably infinite, never read
+    const short2 w = b.kwin[(size_t)group * (G + 1) + g];
+    active = k >= w.x && k <= w.y;
+  }
   const int cand0 = group * CW + lane * CPL;
   int fin[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) fin[c] = 0;
   if (active) {
-    // cell / nk by multiply-high with ceil(2^32/nk): exact for cell < 2^20,
-    // nk < 2^12 (hapt_tables_init bounds both)
-    const int gq = (int)(((unsigned long long)(unsigned)cell * nk_magic) >> 32);
-    const int k = 1 + cell - gq * nk;
-    const int g = s + gq;
     double tm[CPL];
     unsigned cnt2[CPL];
 #pragma unroll
@@ -649,6 +704,9 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.kc = (uint8_t *)(wb + w.kc);
   b.cb_rows = 2 * t->n_meshes;
   for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);
+  b.maxlen = (uint16_t *)(wb + w.maxlen);
+  b.kwin = (short2 *)(wb + w.kwin);
+  b.n_opts = t->n_opts;
   b.H[0] = (double *)(wb + w.H0);
   b.H[1] = (double *)(wb + w.H1);
   b.K[0] = (uint16_t *)(wb + w.K0);
@@ -670,14 +728,18 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     const unsigned gx = grid_for(cells, kWarps);
     const unsigned long long nk = (unsigned long long)(b.L - s + 1);
     const unsigned long long magic = ((1ull << 32) + nk - 1) / nk;  // ceil(2^32 / nk)
+    // the window pass pays off once the layer has far more warps than the
+    // GPU holds at once; on small grids its launch costs more than it saves
+    const int use_window = cells * b.n_groups >= 32768;
+    if (use_window) dp_window<<<b.n_groups, 256, 0, st>>>(b, s);
     for (int g0 = 0; g0 < b.n_groups; g0 += 65535) {
       const int gy = min(65535, b.n_groups - g0);
       if (b.cpl == 1)
-        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
+        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic, use_window);
       else if (b.cpl == 2)
-        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
+        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic, use_window);
       else
-        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
+        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic, use_window);
     }
   }
   HAPT_LAUNCHED("dp_relax");

@@ -262,6 +262,36 @@ int hapt_dag_longest_path(int32_t n_nodes, const int32_t *succ_off,
                           double *makespan, int32_t *processed, void *work,
                           size_t work_bytes, void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* Front end (host code)                                   */
+/* ------------------------------------------------------------------------ */
+
+/* detect_modules (model_graph.py:169-208): partition an operator sequence
+ * into repeated / non-repeated modules.  tag_host [n_ops] = shape_tag ids
+ * (equal tags <=> equal ids), heavy_host [n_ops] = 1 for HEAVY.  Outputs
+ * (capacity n_ops) in position order: span start/end (half-open), group id
+ * (-1 = non_repeated) and occurrence index.  Host memory. */
+int hapt_detect_modules(int32_t n_ops, const int32_t *tag_host, const uint8_t *heavy_host,
+                        int32_t z, int32_t *span_start_host, int32_t *span_end_host,
+                        int32_t *span_group_host, int32_t *span_occ_host,
+                        int32_t *n_spans_host);
+
+/* cluster_layers (model_graph.py:269-333): u layers per module by min-max
+ * flops partition (repeated groups share the first occurrence's cuts).
+ * Outputs (capacity n_ops): op range, flops and param bytes (CPython 3.12
+ * compensated sums, bit-identical), boundary bytes, signature triples
+ * [kind (0 rep, 1 solo), group or solo ordinal, part].  Host memory. */
+int hapt_cluster_layers(int32_t n_ops, const double *flops_host, const double *params_host,
+                        const double *out_bytes_host, int32_t n_spans,
+                        const int32_t *span_start_host, const int32_t *span_end_host,
+                        const int32_t *span_group_host, int32_t u, int32_t *layer_start_host,
+                        int32_t *layer_end_host, double *layer_flops_host,
+                        double *layer_params_host, double *layer_bbytes_host,
+                        int32_t *layer_sig_host, int32_t *n_layers_host);
+
+/* CPython >= 3.12 sum() of n floats (Neumaier), for host-side aggregates. */
+double hapt_py_sum(const double *x_host, int32_t n);
+
 /* FP64 add-throughput probe (roofline denominator for K2/K3): runs `iters`
  * dependent-chain-free DADDs per thread; result[0] = checksum. */
 int hapt_fp64_probe(double *result, int32_t blocks, int32_t threads,

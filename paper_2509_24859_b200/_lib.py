@@ -150,6 +150,13 @@ _SIGNATURES = {
         [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp],
     ),
     "hapt_fp64_probe": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "hapt_detect_modules": (c_i32, [c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "hapt_cluster_layers": (
+        c_i32,
+        [c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
+         c_vp, c_vp],
+    ),
+    "hapt_py_sum": (c_dbl, [c_vp, c_i32]),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -198,9 +205,30 @@ def lib() -> ctypes.CDLL:
     return _handle
 
 
+_host_handle = None
+
+
+def host_lib() -> ctypes.CDLL:
+    """The library for its host-only entry points (the model-graph front end
+    is native C++ host code, like the reference's front end is host Python);
+    no CUDA device needed."""
+    global _host_handle
+    if _host_handle is None:
+        with _lock:
+            if _host_handle is None:
+                _host_handle = _handle if _handle is not None else load()
+    return _host_handle
+
+
 def check(code: int) -> None:
     if code != HAPT_OK:
         msg = lib().hapt_last_error()
+        raise HaptError(code, msg.decode() if msg else "")
+
+
+def check_host(code: int) -> None:
+    if code != HAPT_OK:
+        msg = host_lib().hapt_last_error()
         raise HaptError(code, msg.decode() if msg else "")
 
 

@@ -19,7 +19,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ["hapt_runtime.cu", "hapt_tables.cu", "hapt_dp.cu", "hapt_sim.cu"]
+SOURCES = ["hapt_runtime.cu", "hapt_tables.cu", "hapt_dp.cu", "hapt_sim.cu", "hapt_frontend.cpp"]
 LIB = os.path.join(PKG, "libhapt_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -38,7 +38,7 @@ def flags() -> list[str]:
         "--fmad=false",
         "-std=c++17",
         "-Xcompiler",
-        "-fPIC",
+        "-fPIC,-ffp-contract=off",
         "-Xptxas",
         "-v",
         f"-I{os.path.join(REPO, 'include')}",
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     objs = []
     log = []
     for src in SOURCES:
-        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, os.path.splitext(src)[0] + ".o")
         cmd = [nvcc(), *flags(), *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src),
                "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -55,6 +55,68 @@ def instance(name: str):
             d["num_microbatches"], d["epsilon"])
 
 
+def llama_like_ops(h=8192, s=4096, ffn=28672, vocab=32000, blocks=80, b=1) -> list:
+    """Config D operator list: 3-op prologue, `blocks`
+    x 25-op blocks, 3-op epilogue (2,006 ops); heavy ops carry 2*b*s*in*out
+    flops.  Same recipe as tests/golden/make_golden.py (reference types)."""
+    from .model_graph import HEAVY, LIGHT, OperatorNode
+
+    act = 2.0 * b * s * h
+    light = float(b * s * h)
+    kv = h // 8
+    ops = [(f"embed[{vocab}x{h}]", LIGHT, light, 2.0 * vocab * h),
+           (f"scale[{h}]", LIGHT, light, 0.0),
+           (f"embed_drop[{h}]", LIGHT, light, 0.0)]
+    block = [
+        (f"rms1[{h}]", LIGHT, light, 2.0 * h),
+        (f"q[{h}x{h}]", HEAVY, 2.0 * b * s * h * h, 2.0 * h * h),
+        (f"k[{h}x{kv}]", HEAVY, 2.0 * b * s * h * kv, 2.0 * h * kv),
+        (f"v[{h}x{kv}]", HEAVY, 2.0 * b * s * h * kv, 2.0 * h * kv),
+        (f"rope_q[{h}]", LIGHT, light, 0.0),
+        (f"rope_k[{kv}]", LIGHT, float(b * s * kv), 0.0),
+        (f"score[{s}x{s}]", HEAVY, 2.0 * b * s * s * h, 0.0),
+        (f"mask[{s}]", LIGHT, light, 0.0),
+        (f"softmax[{s}]", LIGHT, light, 0.0),
+        (f"attn_drop[{s}]", LIGHT, light, 0.0),
+        (f"ctx[{s}x{h}]", HEAVY, 2.0 * b * s * s * h, 0.0),
+        (f"o[{h}x{h}]", HEAVY, 2.0 * b * s * h * h, 2.0 * h * h),
+        (f"res1[{h}]", LIGHT, light, 0.0),
+        (f"rms2[{h}]", LIGHT, light, 2.0 * h),
+        (f"gate[{h}x{ffn}]", HEAVY, 2.0 * b * s * h * ffn, 2.0 * h * ffn),
+        (f"up[{h}x{ffn}]", HEAVY, 2.0 * b * s * h * ffn, 2.0 * h * ffn),
+        (f"silu[{ffn}]", LIGHT, float(b * s * ffn), 0.0),
+        (f"mul[{ffn}]", LIGHT, float(b * s * ffn), 0.0),
+        (f"down[{ffn}x{h}]", HEAVY, 2.0 * b * s * ffn * h, 2.0 * ffn * h),
+        (f"res2[{h}]", LIGHT, light, 0.0),
+        (f"cast[{h}]", LIGHT, light, 0.0),
+        (f"drop[{h}]", LIGHT, light, 0.0),
+        (f"stat[{h}]", LIGHT, light, 0.0),
+        (f"id[{h}]", LIGHT, 0.0, 0.0),
+        (f"id[{h}]", LIGHT, 0.0, 0.0),
+    ]
+    ops += block * blocks
+    ops += [(f"final_rms[{h}]", LIGHT, light, 2.0 * h),
+            (f"lm_head[{h}x{vocab}]", HEAVY, 2.0 * b * s * h * vocab, 2.0 * vocab * h),
+            (f"loss[{vocab}]", LIGHT, light, 0.0)]
+    return [OperatorNode(i, kind, fl, pb, act, tag) for i, (tag, kind, fl, pb) in enumerate(ops)]
+
+
+def config_ops(name: str):
+    """(operator list, layers per module unit) of configs A-D (SURVEY.md
+    Appendix B)."""
+    from .model_graph import GptConfig, generate_gpt_sequence
+
+    if name == "A":
+        return generate_gpt_sequence(GptConfig(12, 768, 1024, 1, 50257)), 1
+    if name == "B":
+        return generate_gpt_sequence(GptConfig(24, 2048, 2048, 1, 50257)), 1
+    if name == "C":
+        return generate_gpt_sequence(GptConfig(32, 4096, 4096, 1, 32000)), 3
+    if name.startswith("D"):
+        return llama_like_ops(), int(name[1:])
+    raise KeyError(name)
+
+
 def config_e(n_plans: int, seed: int = 24859):
     """Config E generator: S ~ {2,3,4,6,8}; stage time
     t ~ U(0.5, 2)e-2 s; forward share U(0.3, 0.4); boundary bandwidth

@@ -328,6 +328,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    n_launch0 = lib.hapt_launches()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
@@ -335,6 +336,7 @@ def main():
             step()
             e_ev[i].record()
         torch.cuda.synchronize()
+    n_launched = lib.hapt_launches() - n_launch0  # library's own launch counter
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -350,7 +352,7 @@ def main():
     Lr, G, s_max = tables.L, tables.G, tables.s_max
     relax_launches = sum(1 for s in range(1, s_max + 1) if (Lr - s + 1) * (G - s + 1) > 0)
     chunks = sw.last_chunks
-    launches_per_step = chunks * (2 + relax_launches) + 1
+    launches_per_step = n_launched / args.steps
     nnz = store.dev.nnz
     n_mine = len(mine)
     bytes_per_cand = s_max * 32 * (Lr + 2) * (G + 1) + 28 * nnz
@@ -475,7 +477,7 @@ def main():
         "search_time_s": search_time,
         "search_plan": {"stages": plan.num_stages, "T*": plan.predicted_latency,
                         "t_max": plan.t_max, "evaluated": plan.search_stats["evaluated"]},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": n_launched,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_extras:

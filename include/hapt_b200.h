@@ -64,6 +64,9 @@ enum {
 
 const char *hapt_last_error(void);
 int hapt_version(void);
+/* Kernels this library has enqueued since load (all entry points, all
+   threads): the bench's gpu_launches evidence.  No reference counterpart. */
+int64_t hapt_launches(void);
 
 /* ------------------------------------------------------------------------ */
 /* K1: cost tables                                                           */

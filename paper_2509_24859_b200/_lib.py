@@ -117,6 +117,7 @@ class DpFull(ctypes.Structure):
 _SIGNATURES = {
     "hapt_last_error": (ctypes.c_char_p, []),
     "hapt_version": (c_i32, []),
+    "hapt_launches": (c_i64, []),
     "hapt_tables_bytes": (c_sz, [c_i32, c_i32, c_i32, c_i32]),
     "hapt_tables_init": (c_i32, [ctypes.POINTER(Tables), c_vp, c_sz, c_i32, c_i32, c_i32, c_i32]),
     "hapt_tables_build": (c_i32, [ctypes.POINTER(Tables), ctypes.POINTER(ModelDesc), c_vp]),

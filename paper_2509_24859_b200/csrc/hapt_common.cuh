@@ -20,6 +20,7 @@ constexpr double kInf = __builtin_huge_val();
 constexpr int kKSat = 65535;  // saturation of the integer memory threshold
 
 void set_error(const char *fmt, ...);
+void note_launch();  // one kernel enqueued by the library (hapt_launches)
 void *tables_hist(const hapt_tables *t);  // rank-histogram scratch of a tables buffer
 
 inline int cuda_status(cudaError_t e, const char *what) {

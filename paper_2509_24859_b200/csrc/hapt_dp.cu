@@ -34,6 +34,7 @@ namespace hapt {
 namespace {
 
 constexpr int kWarps = 8;  // warps (cells) per block
+constexpr int kParts = 32;  // copies of the per-candidate state counters
 #ifndef HAPT_RELAX_MINB
 #define HAPT_RELAX_MINB 4  // resident blocks/SM (64 registers, no spills: ptxas -v)
 #endif
@@ -86,8 +87,15 @@ struct Batch {
                        // (state g) is finite for some candidate of the group;
                        // layer s reads [(s-1)%3], writes [s%3], resets [(s+1)%3]
   uint16_t *maxlen;    // [n_groups][n_opts] longest admissible span of an option
-  short2 *kwin;        // [n_groups][G+1] first/last k whose cell can be finite at
-                       // the current layer (dp_window)
+  uint32_t *clist;     // [n_groups][ccap] (g << 16 | k) of the cells inside the
+                       // current layer's windows, group-local compact order
+  size_t ccap;         // L*G >= cells of any layer
+  int32_t *gtot;       // [n_groups] window cells per group
+  int32_t *goff;       // [n_groups+1] exclusive prefix of gtot: the compact cell
+                       // index space dp_relax_compact walks
+  unsigned *ticket;    // dp_window's last-block counter (self-resetting)
+  uint32_t *spart;     // [kParts][n_groups*cw] finite-cell counts of windowed
+                       // layers, spread over kParts copies (dp_states_reduce)
   int n_opts;
   double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
@@ -97,7 +105,8 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], maxlen, kwin, H0, H1, K0, K1, total;
+  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], maxlen, clist, gtot, goff, ticket, spart, H0,
+      H1, K0, K1, total;
 };
 
 WsLayout ws_layout(const hapt_tables *t, int n_cand) {
@@ -116,7 +125,11 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
     cur += align_up(ng * (t->G + 1) * sizeof(int2));
   }
   w.maxlen = cur; cur += align_up(ng * t->n_opts * 2);
-  w.kwin = cur; cur += align_up(ng * (t->G + 1) * sizeof(short2));
+  w.clist = cur; cur += align_up(ng * (size_t)t->L * t->G * 4);
+  w.gtot = cur; cur += align_up(ng * 4);
+  w.goff = cur; cur += align_up((ng + 1) * 4);
+  w.ticket = cur; cur += align_up(4);
+  w.spart = cur; cur += align_up(kParts * np * 4);
   w.H0 = cur; cur += align_up(ng * hg * cw * 8);
   w.H1 = cur; cur += align_up(ng * hg * cw * 8);
   w.K0 = cur; cur += align_up(ng * hg * cw * 2);
@@ -142,6 +155,7 @@ __global__ void dp_prep(Batch b) {
   const int group = blockIdx.x;
   const int cw = b.cw;
   if (threadIdx.x == 0) s_gmax = 0;
+  if (group == 0 && threadIdx.x == 0) *b.ticket = 0u;
   __syncthreads();
   double *H = b.H[0] + (size_t)group * b.hg * cw;
   uint16_t *K = b.K[0] + (size_t)group * b.hg * cw;
@@ -157,6 +171,8 @@ __global__ void dp_prep(Batch b) {
     b.irange[1][(size_t)group * (b.G + 1) + g] = empty;
     b.irange[2][(size_t)group * (b.G + 1) + g] = empty;
   }
+  for (int x = threadIdx.x; x < kParts * cw; x += blockDim.x)
+    b.spart[(size_t)(x / cw) * b.n_groups * cw + (size_t)group * cw + x % cw] = 0u;
   if (threadIdx.x < cw) {
     const int cand = group * cw + threadIdx.x;
     const double tm = b.tmax[cand < b.n_cand ? cand : b.n_cand - 1];
@@ -224,12 +240,44 @@ __global__ void dp_prep(Batch b) {
 // k in [lo - maxlen_o + 1, min(hi, L-s+1)].  Cells outside the hull are
 // provably infinite and are never read by layer s+1 (its read range comes
 // from cells that were finite), so dp_relax skips them without writing.
-__global__ void dp_window(Batch b, int s) {
+// Block-wide exclusive scan of one int per thread (blockDim.x == kWinThreads).
+constexpr int kWinThreads = 256;
+__device__ __forceinline__ int block_excl_scan(int v, int &total) {
+  __shared__ int wsum[kWinThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int before = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < kWinThreads / 32; ++w) {
+    const int x = wsum[w];
+    before += w < warp ? x : 0;
+    total += x;
+  }
+  __syncthreads();  // wsum reusable
+  return before + incl - v;
+}
+
+// Per layer and group: the window [klo, khi] of every state g (cells outside
+// are provably infinite: no option can reach a finite successor from them),
+// the compact enumeration of the cells inside (clist / gtot, then goff by the
+// last block), and the reset of the irange buffer layer s+1 writes (last read
+// by layer s-1).
+__global__ void __launch_bounds__(kWinThreads) dp_window(Batch b, int s) {
   const int group = blockIdx.x;
   const int L = b.L, G = b.G, imax = L - s + 1;
-  for (int g = threadIdx.x; g <= G; g += blockDim.x) {
+  int carry = 0;
+  for (int g0 = 0; g0 <= G; g0 += kWinThreads) {
+    const int g = g0 + threadIdx.x;
     int klo = 0x7fff, khi = 0;
-    if (g >= s) {
+    if (g <= G && g >= s) {
       const int r = b.g_mesh[g], avail = b.g_avail[g];
       for (int o = b.opt_off[r]; o < b.opt_off[r + 1]; ++o) {
         const int devs = b.opt_devs[o], g2 = g - devs;
@@ -243,7 +291,38 @@ __global__ void dp_window(Batch b, int s) {
         khi = max(khi, hi);
       }
     }
-    b.kwin[(size_t)group * (G + 1) + g] = make_short2((short)klo, (short)khi);
+    const int n = khi >= klo ? khi - klo + 1 : 0;
+    int tile;
+    const int off = carry + block_excl_scan(n, tile);
+    if (g <= G) {
+      uint32_t *cl = b.clist + (size_t)group * b.ccap + off;
+      for (int t = 0; t < n; ++t) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t);
+      b.irange[(s + 1) % 3][(size_t)group * (G + 1) + g] = make_int2(0x7fffffff, -1);
+    }
+    carry += tile;
+  }
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    b.gtot[group] = carry;
+    __threadfence();
+    last = atomicAdd(b.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  // last block: exclusive prefix of the group totals
+  __threadfence();
+  int base = 0;
+  for (int j0 = 0; j0 < b.n_groups; j0 += kWinThreads) {
+    const int j = j0 + threadIdx.x;
+    const int v = j < b.n_groups ? __ldcg(b.gtot + j) : 0;
+    int tile;
+    const int off = base + block_excl_scan(v, tile);
+    if (j < b.n_groups) b.goff[j] = off;
+    base += tile;
+  }
+  if (threadIdx.x == 0) {
+    b.goff[b.n_groups] = base;
+    *b.ticket = 0u;
   }
 }
 
@@ -322,9 +401,166 @@ __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
   }
 }
 
+// One DP cell (k, g) of layer s for the 32*CPL candidates of `group`, executed
+// by one warp: fin[c] = whether the cell is finite for candidate c; writes the
+// successor entry of layer s+1 and, for a finite entry, widens irange.
+template <int CPL>
+__device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int k, int g,
+                                           int lane, int4 *__restrict__ stage_e,
+                                           uint16_t *__restrict__ stage_k, int (&fin)[CPL]) {
+  constexpr int CW = 32 * CPL;
+  const int L = b.L, G = b.G;
+  const int cand0 = group * CW + lane * CPL;
+  unsigned cnt2[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) cnt2[c] = (unsigned)b.tcnt[cand0 + c] << 11;
+  const int imax = L - s + 1;
+  const int r = b.g_mesh[g];
+  const int o0 = b.opt_off[r], nopt = b.opt_off[r + 1] - o0;
+  const size_t gbase = (size_t)group * b.hg;
+  const double *Hg = b.H[(s - 1) & 1] + gbase * CW + lane * CPL;
+  const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * CW + lane * CPL;
+  const char *Hb = reinterpret_cast<const char *>(Hg);
+  const char *Kb = reinterpret_cast<const char *>(Kg);
+  double bv[CPL];
+  unsigned bw2[CPL], bw3[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    bv[c] = kInf;
+    bw2[c] = ~0u;
+    bw3[c] = 0;
+  }
+  // options of mesh r, 32 at a time (a mesh rarely has more than 32 submesh
+  // shapes); rows are visited in ascending option order
+  for (int c0 = 0; c0 < nopt; c0 += 32) {
+    const int nch = min(32, nopt - c0);
+    // lane j: admissible entries of option o0+c0+j's row (k) at this layer
+    int len = 0, beg = 0, hbase = 0;
+    bool needkk = false;
+    if (lane < nch) {
+      const int o = o0 + c0 + lane;
+      const int devs = b.opt_devs[o], g2 = g - devs;
+      if (devs <= b.g_avail[g] && g2 >= s - 1) {
+        const int row = o * (L + 2) + k;
+        // admissible splits: i <= L-s+1 (later successors are provably
+        // infinite), inside the range where state g2's successor entry is
+        // finite for some candidate of the group, and before the group's
+        // suffix-rank cut -- every skipped entry is one the reference
+        // skips for all these candidates (fc == inf or tt > t_max)
+        const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
+        const int lo_i = max(k, fr.x), hi_i = min(imax, fr.y);
+        if (lo_i <= hi_i) {
+          const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
+          const int a = pos[lo_i - 1];
+          const int z = min((int)pos[hi_i], (int)b.cut_sr[(size_t)group * b.rows + row]);
+          beg = b.span_off[row] + a;
+          len = max(0, z - a);
+        }
+        hbase = g2 * (L + 1);
+        // KK <= 3s at layer s: ceil(2c/t_max) <= 2 and N grows by <= 3 per
+        // stage, so a row whose thresholds are all >= 3s cannot fail the
+        // memory mask (_dp.pyx:83)
+        needkk = len > 0 && (int)b.row_kmin[row] < 3 * s;
+      }
+    }
+    int incl = len;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    const int T = __shfl_sync(0xffffffffu, incl, 31);
+    const int start = incl - len;
+    const bool anykk = __any_sync(0xffffffffu, needkk);
+    for (int r0 = 0; r0 < T; r0 += 32) {
+      const int t = r0 + lane;
+      int j = 0;  // owner row: number of rows whose entries end at or before t
+      for (int q = 0; q < nch; ++q) j += (__shfl_sync(0xffffffffu, incl, q) <= t);
+      const int jj = min(j, 31);
+      const int ob = __shfl_sync(0xffffffffu, beg, jj);
+      const int os = __shfl_sync(0xffffffffu, start, jj);
+      const int oh = __shfl_sync(0xffffffffu, hbase, jj);
+      int4 se = make_int4(0, 0, -1, 0);  // inert padding entry
+      uint16_t sk = 0;
+      if (t < T) {
+        const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
+        const unsigned w2 =
+            x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
+        se = make_int4(x.x, x.y, (int)w2, (oh + (x.w & 0xffff)) * (256 * CPL));
+        sk = (uint16_t)((unsigned)x.w >> 16);
+      }
+      stage_e[lane] = se;
+      stage_k[lane] = sk;
+      __syncwarp();
+      const int n = min(32, T - r0);
+      if (anykk)
+        relax_entries<true, CPL>(stage_e, stage_k, n, cnt2, Hb, Kb, bv, bw2, bw3);
+      else
+        relax_entries<false, CPL>(stage_e, stage_k, n, cnt2, Hb, Kb, bv, bw2, bw3);
+      __syncwarp();
+    }
+  }
+  // epilogue per candidate
+  double hn[CPL];
+  int kn[CPL];
+  const int crow = b.g_crow[g];
+  const double c2 = crow >= 0 ? __dmul_rn(2.0, b.cb[(size_t)crow * (L + 1) + (k - 1)]) : 0.0;
+  const uint8_t *kcp = b.kc + ((size_t)group * b.cb_rows + (crow >= 0 ? crow : 0)) * (L + 1) * CW +
+                       (size_t)(k - 1) * CW + lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    fin[c] = bw2[c] != ~0u;
+    const double best = bv[c];
+    const int bo = (int)(bw2[c] & 2047u), boff = (int)(bw3[c] / (256u * CPL));
+    // split i of the winner: its successor offset minus the row of g2 = g - devs
+    const int bi = fin[c] ? boff - (g - b.opt_devs[bo]) * (L + 1) : 0;
+    // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
+    const int bkk = fin[c] ? (int)__ldg(Kg + (size_t)boff * CW + c) : 0;
+    const int cand = cand0 + c;
+    if (cand < b.n_cand) {
+      if (k == 1 && g == G) {
+        b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
+        if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
+      }
+      if (fin[c]) {
+        const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
+        if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
+        if (b.full.bp_o) {
+          if (b.full.F) b.full.F[e] = best;
+          if (b.full.N) b.full.N[e] = (double)bkk;
+          b.full.bp_i[e] = bi;
+          b.full.bp_o[e] = bo;
+        }
+      }
+    }
+    // successor entry (state g, split i = k-1) for layer s+1:
+    // H = 2c + F, KK = (ceil(2c/t_max) + 1) + N, or +inf if c > t_max
+    hn[c] = kInf;
+    kn[c] = 0;
+    const int kcv = crow >= 0 ? (int)kcp[c] : 0xFF;
+    if (fin[c] && kcv != 0xFF) {
+      hn[c] = __dadd_rn(c2, best);
+      kn[c] = kcv + bkk;
+    }
+  }
+  const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
+  bool anyfin = false;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    b.H[s & 1][o_idx + c] = hn[c];
+    b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
+    anyfin |= hn[c] != kInf;
+  }
+  if (__any_sync(0xffffffffu, anyfin) && lane == 0) {
+    int2 *fr = &b.irange[s % 3][(size_t)group * (G + 1) + g];
+    atomicMin(&fr->x, k - 1);
+    atomicMax(&fr->y, k - 1);
+  }
+}
+
 template <int CPL>
 __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
-    dp_relax(Batch b, int s, int group0, unsigned long long nk_magic, int use_window) {
+    dp_relax(Batch b, int s, int group0, unsigned long long nk_magic) {
   constexpr int CW = 32 * CPL;
   __shared__ int fin_cnt[kWarps][CW];
   __shared__ int4 stage_e[kWarps][32];
@@ -339,166 +575,11 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   const int gq = (int)(((unsigned long long)(unsigned)cell * nk_magic) >> 32);
   const int k = 1 + cell - gq * nk;
   const int g = s + gq;
-  bool active = cell < nk * ng;
-  if (active && use_window) {  // outside the window: provably infinite, never read
-    const short2 w = b.kwin[(size_t)group * (G + 1) + g];
-    active = k >= w.x && k <= w.y;
-  }
-  const int cand0 = group * CW + lane * CPL;
+  const bool active = cell < nk * ng;
   int fin[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) fin[c] = 0;
-  if (active) {
-    double tm[CPL];
-    unsigned cnt2[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      tm[c] = b.tmax_pad[cand0 + c];
-      cnt2[c] = (unsigned)b.tcnt[cand0 + c] << 11;
-    }
-    const int imax = L - s + 1;
-    const int r = b.g_mesh[g];
-    const int o0 = b.opt_off[r], nopt = b.opt_off[r + 1] - o0;
-    const size_t gbase = (size_t)group * b.hg;
-    const double *Hg = b.H[(s - 1) & 1] + gbase * CW + lane * CPL;
-    const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * CW + lane * CPL;
-    const char *Hb = reinterpret_cast<const char *>(Hg);
-    const char *Kb = reinterpret_cast<const char *>(Kg);
-    double bv[CPL];
-    unsigned bw2[CPL], bw3[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      bv[c] = kInf;
-      bw2[c] = ~0u;
-      bw3[c] = 0;
-    }
-    // options of mesh r, 32 at a time (a mesh rarely has more than 32 submesh
-    // shapes); rows are visited in ascending option order
-    for (int c0 = 0; c0 < nopt; c0 += 32) {
-      const int nch = min(32, nopt - c0);
-      // lane j: admissible entries of option o0+c0+j's row (k) at this layer
-      int len = 0, beg = 0, hbase = 0;
-      bool needkk = false;
-      if (lane < nch) {
-        const int o = o0 + c0 + lane;
-        const int devs = b.opt_devs[o], g2 = g - devs;
-        if (devs <= b.g_avail[g] && g2 >= s - 1) {
-          const int row = o * (L + 2) + k;
-          // admissible splits: i <= L-s+1 (later successors are provably
-          // infinite), inside the range where state g2's successor entry is
-          // finite for some candidate of the group, and before the group's
-          // suffix-rank cut -- every skipped entry is one the reference
-          // skips for all these candidates (fc == inf or tt > t_max)
-          const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
-          const int lo_i = max(k, fr.x), hi_i = min(imax, fr.y);
-          if (lo_i <= hi_i) {
-            const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
-            const int a = pos[lo_i - 1];
-            const int z = min((int)pos[hi_i], (int)b.cut_sr[(size_t)group * b.rows + row]);
-            beg = b.span_off[row] + a;
-            len = max(0, z - a);
-          }
-          hbase = g2 * (L + 1);
-          // KK <= 3s at layer s: ceil(2c/t_max) <= 2 and N grows by <= 3 per
-          // stage, so a row whose thresholds are all >= 3s cannot fail the
-          // memory mask (_dp.pyx:83)
-          needkk = len > 0 && (int)b.row_kmin[row] < 3 * s;
-        }
-      }
-      int incl = len;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += v;
-      }
-      const int T = __shfl_sync(0xffffffffu, incl, 31);
-      const int start = incl - len;
-      const bool anykk = __any_sync(0xffffffffu, needkk);
-      for (int r0 = 0; r0 < T; r0 += 32) {
-        const int t = r0 + lane;
-        int j = 0;  // owner row: number of rows whose entries end at or before t
-        for (int q = 0; q < nch; ++q) j += (__shfl_sync(0xffffffffu, incl, q) <= t);
-        const int jj = min(j, 31);
-        const int ob = __shfl_sync(0xffffffffu, beg, jj);
-        const int os = __shfl_sync(0xffffffffu, start, jj);
-        const int oh = __shfl_sync(0xffffffffu, hbase, jj);
-        int4 se = make_int4(0, 0, -1, 0);  // inert padding entry
-        uint16_t sk = 0;
-        if (t < T) {
-          const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
-          const unsigned w2 =
-              x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
-          se = make_int4(x.x, x.y, (int)w2, (oh + (x.w & 0xffff)) * (256 * CPL));
-          sk = (uint16_t)((unsigned)x.w >> 16);
-        }
-        stage_e[warp][lane] = se;
-        stage_k[warp][lane] = sk;
-        __syncwarp();
-        const int n = min(32, T - r0);
-        if (anykk)
-          relax_entries<true, CPL>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
-        else
-          relax_entries<false, CPL>(stage_e[warp], stage_k[warp], n, cnt2, Hb, Kb, bv, bw2, bw3);
-        __syncwarp();
-      }
-    }
-    // epilogue per candidate
-    double hn[CPL];
-    int kn[CPL];
-    const int crow = b.g_crow[g];
-    const double c2 = crow >= 0 ? __dmul_rn(2.0, b.cb[(size_t)crow * (L + 1) + (k - 1)]) : 0.0;
-    const uint8_t *kcp = b.kc + ((size_t)group * b.cb_rows + (crow >= 0 ? crow : 0)) * (L + 1) * CW +
-                         (size_t)(k - 1) * CW + lane * CPL;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      fin[c] = bw2[c] != ~0u;
-      const double best = bv[c];
-      const int bo = (int)(bw2[c] & 2047u), boff = (int)(bw3[c] / (256u * CPL));
-      // split i of the winner: its successor offset minus the row of g2 = g - devs
-      const int bi = fin[c] ? boff - (g - b.opt_devs[bo]) * (L + 1) : 0;
-      // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
-      const int bkk = fin[c] ? (int)__ldg(Kg + (size_t)boff * CW + c) : 0;
-      const int cand = cand0 + c;
-      if (cand < b.n_cand) {
-        if (k == 1 && g == G) {
-          b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
-          if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
-        }
-        if (fin[c]) {
-          const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
-          if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
-          if (b.full.bp_o) {
-            if (b.full.F) b.full.F[e] = best;
-            if (b.full.N) b.full.N[e] = (double)bkk;
-            b.full.bp_i[e] = bi;
-            b.full.bp_o[e] = bo;
-          }
-        }
-      }
-      // successor entry (state g, split i = k-1) for layer s+1:
-      // H = 2c + F, KK = (ceil(2c/t_max) + 1) + N, or +inf if c > t_max
-      hn[c] = kInf;
-      kn[c] = 0;
-      const int kcv = crow >= 0 ? (int)kcp[c] : 0xFF;
-      if (fin[c] && kcv != 0xFF) {
-        hn[c] = __dadd_rn(c2, best);
-        kn[c] = kcv + bkk;
-      }
-    }
-    const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
-    bool anyfin = false;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      b.H[s & 1][o_idx + c] = hn[c];
-      b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
-      anyfin |= hn[c] != kInf;
-    }
-    if (__any_sync(0xffffffffu, anyfin) && lane == 0) {
-      int2 *fr = &b.irange[s % 3][(size_t)group * (G + 1) + g];
-      atomicMin(&fr->x, k - 1);
-      atomicMax(&fr->y, k - 1);
-    }
-  }
+  if (active) relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
   if (blockIdx.x == 0) {  // the buffer layer s+1 writes: last read by layer s-1
     for (int x = threadIdx.x; x <= G; x += blockDim.x)
       b.irange[(s + 1) % 3][(size_t)group * (G + 1) + x] = make_int2(0x7fffffff, -1);
@@ -512,6 +593,97 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     for (int w = 0; w < kWarps; ++w) sum += fin_cnt[w][x];
     const int cand = group * CW + x;
     if (sum && cand < b.n_cand) atomicAdd(&b.states[cand], (unsigned long long)sum);
+  }
+}
+
+// Warp-collective: the group owning compact cell idx = largest j < ng with
+// goff[j] <= idx (goff non-decreasing, goff[0] = 0), 32 entries per step.
+__device__ __forceinline__ int find_group(const int32_t *__restrict__ goff, int ng, int idx,
+                                          int lane) {
+  for (int base = 0;; base += 32) {
+    const int j = base + 1 + lane;
+    const bool le = j < ng && __ldg(goff + j) <= idx;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    if (m != 0xffffffffu) return base + __popc(m);
+  }
+}
+
+// Windowed layers: only the cells inside dp_window's windows, enumerated
+// compactly (group-major, then g, then k), one warp per cell over an
+// upper-bound grid (surplus blocks exit at once) -- no warp is spent on a
+// provably infinite cell.  Finite-cell counts are combined per block in
+// shared memory and flushed by whichever warp finishes last, so no warp waits
+// at a barrier for a slower one; the flush goes to one of kParts counter
+// copies (dp_states_reduce sums them) to avoid a same-address atomic hot spot.
+template <int CPL>
+__global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
+    dp_relax_compact(Batch b, int s) {
+  constexpr int CW = 32 * CPL;
+  __shared__ int4 stage_e[kWarps][32];
+  __shared__ uint16_t stage_k[kWarps][32];
+  __shared__ unsigned s_cnt[2][CW];  // the block's first group and the next
+  __shared__ unsigned s_done;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = b.G;
+  const int total = b.goff[b.n_groups];
+  const int idx0 = blockIdx.x * kWarps;
+  if (idx0 >= total) return;  // whole block past the compact range
+  for (int x = threadIdx.x; x < 2 * CW; x += blockDim.x) (&s_cnt[0][0])[x] = 0u;
+  if (threadIdx.x == 0) s_done = 0u;
+  __syncthreads();
+  const int group0 = find_group(b.goff, b.n_groups, idx0, lane);
+  const int idx = idx0 + warp;
+  if (idx < total) {
+    const int group = find_group(b.goff, b.n_groups, idx, lane);
+    const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
+    const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
+    int fin[CPL];
+    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
+    const int slot = group - group0;  // a block spans 8 cells: almost always 0 or 1
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      if (!fin[c]) continue;
+      if (slot < 2)
+        atomicAdd(&s_cnt[slot][lane * CPL + c], 1u);
+      else  // third group inside one block (tiny groups): straight to a copy
+        atomicAdd(b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW +
+                      (size_t)group * CW + lane * CPL + c, 1u);
+    }
+  }
+  __threadfence_block();
+  unsigned done = 0;
+  if (lane == 0) done = atomicAdd(&s_done, 1u);
+  done = __shfl_sync(0xffffffffu, done, 0);
+  if (done != kWarps - 1) return;
+  // last warp of the block: flush both slots
+  __threadfence_block();
+  uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
+  for (int slot = 0; slot < 2 && group0 + slot < b.n_groups; ++slot) {
+    uint32_t *dst = part + (size_t)(group0 + slot) * CW + lane * CPL;
+    const volatile unsigned *src = &s_cnt[slot][lane * CPL];
+    if constexpr (CPL == 1) {
+      if (src[0]) atomicAdd(dst, src[0]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; c += 2) {
+        const unsigned lo = src[c], hi = src[c + 1];
+        if (lo | hi)
+          atomicAdd(reinterpret_cast<unsigned long long *>(dst + c),
+                    (unsigned long long)lo | ((unsigned long long)hi << 32));
+      }
+    }
+  }
+}
+
+// states[cand] += sum of the kParts partial counters (padding lanes dropped)
+__global__ void dp_states_reduce(Batch b) {
+  const int np = b.n_groups * b.cw;
+  for (int cand = blockIdx.x * blockDim.x + threadIdx.x; cand < b.n_cand;
+       cand += gridDim.x * blockDim.x) {
+    unsigned long long sum = 0;
+#pragma unroll 8
+    for (int q = 0; q < kParts; ++q) sum += b.spart[(size_t)q * np + cand];
+    if (sum) b.states[cand] += sum;
   }
 }
 
@@ -705,7 +877,12 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.cb_rows = 2 * t->n_meshes;
   for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);
   b.maxlen = (uint16_t *)(wb + w.maxlen);
-  b.kwin = (short2 *)(wb + w.kwin);
+  b.clist = (uint32_t *)(wb + w.clist);
+  b.ccap = (size_t)t->L * t->G;
+  b.gtot = (int32_t *)(wb + w.gtot);
+  b.goff = (int32_t *)(wb + w.goff);
+  b.ticket = (unsigned *)(wb + w.ticket);
+  b.spart = (uint32_t *)(wb + w.spart);
   b.n_opts = t->n_opts;
   b.H[0] = (double *)(wb + w.H0);
   b.H[1] = (double *)(wb + w.H1);
@@ -719,8 +896,8 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
 
 int run_sweep(const Batch &b, cudaStream_t st) {
   dp_ftop_init<<<grid_for((size_t)b.n_cand * (b.s_max + 1), 256), 256, 0, st>>>(
-      b.ftop, b.states, b.n_cand, b.s_max);
-  dp_prep<<<b.n_groups, 256, 0, st>>>(b);  // block >= 128 = max group width
+      b.ftop, b.states, b.n_cand, b.s_max); ::hapt::note_launch();
+  dp_prep<<<b.n_groups, 256, 0, st>>>(b); ::hapt::note_launch();  // block >= 128 = max group width
   HAPT_LAUNCHED("dp_prep");
   for (int s = 1; s <= b.s_max; ++s) {
     const long cells = (long)(b.L - s + 1) * (b.G - s + 1);
@@ -731,17 +908,31 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     // the window pass pays off once the layer has far more warps than the
     // GPU holds at once; on small grids its launch costs more than it saves
     const int use_window = cells * b.n_groups >= 32768;
-    if (use_window) dp_window<<<b.n_groups, 256, 0, st>>>(b, s);
+    if (use_window) {
+      dp_window<<<b.n_groups, kWinThreads, 0, st>>>(b, s); ::hapt::note_launch();
+      const unsigned cgrid = grid_for((size_t)cells * b.n_groups, kWarps);
+      if (b.cpl == 1)
+        dp_relax_compact<1><<<cgrid, kWarps * 32, 0, st>>>(b, s);
+      else if (b.cpl == 2)
+        dp_relax_compact<2><<<cgrid, kWarps * 32, 0, st>>>(b, s);
+      else
+        dp_relax_compact<4><<<cgrid, kWarps * 32, 0, st>>>(b, s);
+      ::hapt::note_launch();
+      continue;
+    }
     for (int g0 = 0; g0 < b.n_groups; g0 += 65535) {
       const int gy = min(65535, b.n_groups - g0);
       if (b.cpl == 1)
-        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic, use_window);
+        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
       else if (b.cpl == 2)
-        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic, use_window);
+        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
       else
-        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic, use_window);
+        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
+      ::hapt::note_launch();
     }
   }
+  dp_states_reduce<<<grid_for(b.n_cand, 256), 256, 0, st>>>(b);
+  ::hapt::note_launch();
   HAPT_LAUNCHED("dp_relax");
   return HAPT_OK;
 }
@@ -785,7 +976,7 @@ extern "C" int hapt_dp_select(const double *ftop, const double *tmax, int32_t n_
   }
   dp_select<<<1, 1024, 0, (cudaStream_t)stream>>>(ftop, tmax, n_cand, s_max,
                                                    (long long)num_microbatches, tstar,
-                                                   best_s, winner);
+                                                   best_s, winner); ::hapt::note_launch();
   HAPT_LAUNCHED("dp_select");
   return HAPT_OK;
 }
@@ -838,14 +1029,14 @@ extern "C" int hapt_dp_backtrack(const hapt_tables *t, double tmax, int32_t best
   full.bp_i = (int32_t *)(w + y.bpi);
   full.bp_o = (int32_t *)(w + y.bpo);
   const size_t cells = (size_t)(t->s_max + 1) * (t->L + 2) * (t->G + 1);
-  fill_full<<<grid_for(cells, 256), 256, 0, st>>>(full, cells, t->L, t->G);
+  fill_full<<<grid_for(cells, 256), 256, 0, st>>>(full, cells, t->L, t->G); ::hapt::note_launch();
   Batch b = make_batch(t, d_tmax, 1, (double *)(w + y.ftop), (int64_t *)(w + y.states), &full,
                        w + y.ws);
   int rc = run_sweep(b, st);
   if (rc != HAPT_OK) return rc;
   int32_t *err = (int32_t *)(w + y.err);
   dp_walk<<<1, 32, 0, st>>>(full, t->opt_devs, t->L, t->G, t->s_max, best_s, stages, kchain,
-                            n_stages, err);
+                            n_stages, err); ::hapt::note_launch();
   HAPT_LAUNCHED("dp_walk");
   int32_t herr = 0;
   HAPT_CUDA(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
@@ -865,7 +1056,7 @@ extern "C" int hapt_dp_walk(const hapt_tables *t, const int32_t *bp_cand, int32_
     return HAPT_EINVAL;
   }
   dp_walk_packed<<<1, 32, 0, (cudaStream_t)stream>>>(bp_cand, t->opt_devs, t->L, t->G, best_s,
-                                                     stages, n_stages);
+                                                     stages, n_stages); ::hapt::note_launch();
   HAPT_LAUNCHED("dp_walk_packed");
   return HAPT_OK;
 }
@@ -880,8 +1071,8 @@ extern "C" int hapt_activated_pairs(const hapt_tables *t, const double *tmax, in
   // the rank histogram lives in the tables scratch
   unsigned long long *hist = (unsigned long long *)tables_hist(t);
   HAPT_CUDA(cudaMemsetAsync(hist, 0, ((size_t)t->pool_cap + 1) * 8, st));
-  k_rank_hist<<<grid_for(t->nnz_cap, 256), 256, 0, st>>>(t->spans, t->counters, hist);
-  k_activated<<<1, 1024, 0, st>>>(t->pool, t->counters, hist, tmax, n_cand, activated);
+  k_rank_hist<<<grid_for(t->nnz_cap, 256), 256, 0, st>>>(t->spans, t->counters, hist); ::hapt::note_launch();
+  k_activated<<<1, 1024, 0, st>>>(t->pool, t->counters, hist, tmax, n_cand, activated); ::hapt::note_launch();
   HAPT_LAUNCHED("hapt_activated_pairs");
   return HAPT_OK;
 }

@@ -3,6 +3,8 @@
 // vector peak is not part of MEASURED_PEAKS.json, so bench.py measures it.
 #include <stdarg.h>
 
+#include <atomic>
+
 #include "hapt_common.cuh"
 
 namespace hapt {
@@ -15,6 +17,10 @@ void set_error(const char *fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
+
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 // 8 independent DADD chains per thread; iters * 8 adds per thread.
@@ -39,13 +45,15 @@ extern "C" const char *hapt_last_error(void) { return g_err; }
 
 extern "C" int hapt_version(void) { return 10000; }
 
+extern "C" int64_t hapt_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
 extern "C" int hapt_fp64_probe(double *result, int32_t blocks, int32_t threads, int32_t iters,
                                void *stream) {
   if (!result || blocks < 1 || threads < 32 || iters < 1) {
     set_error("hapt_fp64_probe: invalid arguments");
     return HAPT_EINVAL;
   }
-  k_fp64_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(result, iters);
+  k_fp64_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>(result, iters); ::hapt::note_launch();
   HAPT_LAUNCHED("k_fp64_probe");
   return HAPT_OK;
 }

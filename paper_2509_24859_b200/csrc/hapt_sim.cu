@@ -474,7 +474,7 @@ void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const do
     attr = true;
   }
   k_sim_s<S><<<grid_for(n, C::threads), C::threads, C::smem, st>>>(
-      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status);
+      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status); ::hapt::note_launch();
 }
 
 }  // namespace
@@ -492,7 +492,7 @@ extern "C" int hapt_launch_counts(int32_t n_plans, const int32_t *stage_off, con
     return HAPT_EINVAL;
   }
   k_counts<<<grid_for(n_plans, 128), 128, 0, (cudaStream_t)stream>>>(
-      n_plans, stage_off, t_fwd, t_bwd, comm, tmax, epsilon, kind, counts, status);
+      n_plans, stage_off, t_fwd, t_bwd, comm, tmax, epsilon, kind, counts, status); ::hapt::note_launch();
   HAPT_LAUNCHED("k_counts");
   return HAPT_OK;
 }
@@ -540,14 +540,14 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
     k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, nullptr, nullptr, stage_off, t_fwd,
                                                   t_bwd, comm, counts, num_mb, makespan,
                                                   node_start, node_end, node_off, ring_depth,
-                                                  ring, status);
+                                                  ring, status); ::hapt::note_launch();
     HAPT_LAUNCHED("k_sim");
     return HAPT_OK;
   }
   const int nb = (n_plans + kBucketBlock - 1) / kBucketBlock;
-  k_bucket_hist<<<nb, kBucketBlock, 0, st>>>(n_plans, stage_off, bhist);
-  k_bucket_scan<<<1, 32, 0, st>>>(nb, bhist, cnt);
-  k_bucket_scatter<<<nb, kBucketBlock, 0, st>>>(n_plans, stage_off, bhist, cnt, perm);
+  k_bucket_hist<<<nb, kBucketBlock, 0, st>>>(n_plans, stage_off, bhist); ::hapt::note_launch();
+  k_bucket_scan<<<1, 32, 0, st>>>(nb, bhist, cnt); ::hapt::note_launch();
+  k_bucket_scatter<<<nb, kBucketBlock, 0, st>>>(n_plans, stage_off, bhist, cnt, perm); ::hapt::note_launch();
   int32_t h[19];  // [0..8] bucket sizes, [10..18] bucket starts in perm
   HAPT_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
   HAPT_CUDA(cudaStreamSynchronize(st));
@@ -582,15 +582,17 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   // plans with S > 8 (bucket 0 = perm[0..h[0])) and any plan the fast path
   // handed back (appended after bucket 0) go through the generic walk
   HAPT_CUDA(cudaMemsetAsync(cnt + 20, 0, 4, st));
-  if (h[0] > 0)
+  if (h[0] > 0) {
     k_sim<<<grid_for(h[0], 128), 128, 0, st>>>(h[0], perm, cnt + 0, stage_off, t_fwd, t_bwd,
                                                comm, counts, num_mb, makespan, nullptr, nullptr,
                                                nullptr, ring_depth, ring, status);
-  k_sim_retry<<<grid_for(n_plans, 256), 256, 0, st>>>(n_plans, status, perm + h[0], cnt + 20);
+    ::hapt::note_launch();
+  }
+  k_sim_retry<<<grid_for(n_plans, 256), 256, 0, st>>>(n_plans, status, perm + h[0], cnt + 20); ::hapt::note_launch();
   k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, perm + h[0], cnt + 20, stage_off,
                                                 t_fwd, t_bwd, comm, counts, num_mb, makespan,
                                                 nullptr, nullptr, nullptr, ring_depth, ring,
-                                                status);
+                                                status); ::hapt::note_launch();
   HAPT_LAUNCHED("k_sim");
   return HAPT_OK;
 }
@@ -613,7 +615,7 @@ extern "C" int hapt_dag_longest_path(int32_t n_nodes, const int32_t *succ_off,
   char *w = (char *)work;
   k_dag<<<1, 1024, 0, (cudaStream_t)stream>>>(n_nodes, succ_off, succ_idx, indeg, duration,
                                                start, end, makespan, processed, (int32_t *)w,
-                                               (int32_t *)(w + a), (int32_t *)(w + 2 * a));
+                                               (int32_t *)(w + a), (int32_t *)(w + 2 * a)); ::hapt::note_launch();
   HAPT_LAUNCHED("k_dag");
   return HAPT_OK;
 }

@@ -434,8 +434,8 @@ int finalize_impl(hapt_tables *tp, cudaStream_t st) {
   Scratch s = scratch_of(&t);
   Layout y = layout(t.L, t.G, t.n_opts, t.n_meshes);
   const size_t rows = y.rows;
-  k_fill_keys<<<grid_for(y.nnz_cap, 256), 256, 0, st>>>(s.keys_a, y.nnz_cap);
-  k_span_meta<<<grid_for(rows, 128), 128, 0, st>>>(t, s.keys_a);
+  k_fill_keys<<<grid_for(y.nnz_cap, 256), 256, 0, st>>>(s.keys_a, y.nnz_cap); ::hapt::note_launch();
+  k_span_meta<<<grid_for(rows, 128), 128, 0, st>>>(t, s.keys_a); ::hapt::note_launch();
   HAPT_LAUNCHED("k_span_meta");
   cub::DoubleBuffer<unsigned long long> db(s.keys_a, s.keys_b);
   size_t need = 0;
@@ -455,10 +455,10 @@ int finalize_impl(hapt_tables *tp, cudaStream_t st) {
     return HAPT_ENOSPACE;
   }
   HAPT_CUDA(cub::DeviceSelect::Unique(s.cub_temp, need, sorted, uniq, num_unique, (int)y.nnz_cap, st));
-  k_pool_decode<<<grid_for(y.pool_cap, 256), 256, 0, st>>>(t, uniq, num_unique);
-  k_prank<<<grid_for(y.nnz_cap, 256), 256, 0, st>>>(t);
-  k_srank<<<grid_for(rows, 128), 128, 0, st>>>(t);
-  k_gcrow<<<grid_for(t.G + 1, 128), 128, 0, st>>>(t);
+  k_pool_decode<<<grid_for(y.pool_cap, 256), 256, 0, st>>>(t, uniq, num_unique); ::hapt::note_launch();
+  k_prank<<<grid_for(y.nnz_cap, 256), 256, 0, st>>>(t); ::hapt::note_launch();
+  k_srank<<<grid_for(rows, 128), 128, 0, st>>>(t); ::hapt::note_launch();
+  k_gcrow<<<grid_for(t.G + 1, 128), 128, 0, st>>>(t); ::hapt::note_launch();
   HAPT_LAUNCHED("finalize");
   return HAPT_OK;
 }
@@ -551,12 +551,12 @@ extern "C" int hapt_tables_build(hapt_tables *t, const hapt_model_desc *d, void 
   const int L = t->L;
   HAPT_CUDA(cudaMemsetAsync(t->counters, 0, 16 * 8, st));
   HAPT_CUDA(cudaMemsetAsync(s.lcp, 0, (size_t)(L + 2) * (L + 2) * 4, st));
-  k1_meta<<<1, 256, 0, st>>>(*t, *d, s.prefix);
-  k1_lcp<<<grid_for(L, 128), 128, 0, st>>>(d->layer_sig, L, s.lcp);
-  k1_canon<<<grid_for((size_t)(L + 2) * (L + 2), 256), 256, 0, st>>>(L, d->dedup, s.lcp, t->canon_q);
-  k1_profile<<<grid_for(y.cells, 256), 256, 0, st>>>(*t, *d, s.prefix);
+  k1_meta<<<1, 256, 0, st>>>(*t, *d, s.prefix); ::hapt::note_launch();
+  k1_lcp<<<grid_for(L, 128), 128, 0, st>>>(d->layer_sig, L, s.lcp); ::hapt::note_launch();
+  k1_canon<<<grid_for((size_t)(L + 2) * (L + 2), 256), 256, 0, st>>>(L, d->dedup, s.lcp, t->canon_q); ::hapt::note_launch();
+  k1_profile<<<grid_for(y.cells, 256), 256, 0, st>>>(*t, *d, s.prefix); ::hapt::note_launch();
   HAPT_LAUNCHED("k1_profile");
-  k_row_count<<<grid_for(y.rows + 1, 128), 128, 0, st>>>(*t, s.row_cnt);
+  k_row_count<<<grid_for(y.rows + 1, 128), 128, 0, st>>>(*t, s.row_cnt); ::hapt::note_launch();
   size_t need = 0;
   HAPT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, s.row_cnt, t->span_off, (int)(y.rows + 1), st));
   if (need > s.cub_bytes) {
@@ -564,7 +564,7 @@ extern "C" int hapt_tables_build(hapt_tables *t, const hapt_model_desc *d, void 
     return HAPT_ENOSPACE;
   }
   HAPT_CUDA(cub::DeviceScan::ExclusiveSum(s.cub_temp, need, s.row_cnt, t->span_off, (int)(y.rows + 1), st));
-  k_row_fill<<<grid_for(y.rows, 128), 128, 0, st>>>(*t);
+  k_row_fill<<<grid_for(y.rows, 128), 128, 0, st>>>(*t); ::hapt::note_launch();
   HAPT_LAUNCHED("k_row_fill");
   return finalize_impl(t, st);
 }

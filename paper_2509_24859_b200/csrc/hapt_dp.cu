@@ -474,8 +474,15 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     const bool anykk = __any_sync(0xffffffffu, needkk);
     for (int r0 = 0; r0 < T; r0 += 32) {
       const int t = r0 + lane;
-      int j = 0;  // owner row: number of rows whose entries end at or before t
-      for (int q = 0; q < nch; ++q) j += (__shfl_sync(0xffffffffu, incl, q) <= t);
+      // owner row: number of rows whose entries end at or before t, by binary
+      // search over the lanes' inclusive ends (non-decreasing; rows past nch
+      // end at T > t for every real entry)
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, j + step - 1);
+        if (v <= t) j += step;
+      }
       const int jj = min(j, 31);
       const int ob = __shfl_sync(0xffffffffu, beg, jj);
       const int os = __shfl_sync(0xffffffffu, start, jj);
@@ -507,30 +514,32 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   const double c2 = crow >= 0 ? __dmul_rn(2.0, b.cb[(size_t)crow * (L + 1) + (k - 1)]) : 0.0;
   const uint8_t *kcp = b.kc + ((size_t)group * b.cb_rows + (crow >= 0 ? crow : 0)) * (L + 1) * CW +
                        (size_t)(k - 1) * CW + lane * CPL;
+  // warp-uniform: backpointers / F / N are only recorded when a caller asked
+  const bool want_bp = b.full.bp_packed != nullptr || b.full.bp_o != nullptr;
+  const bool top = k == 1 && g == G;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     fin[c] = bw2[c] != ~0u;
     const double best = bv[c];
-    const int bo = (int)(bw2[c] & 2047u), boff = (int)(bw3[c] / (256u * CPL));
-    // split i of the winner: its successor offset minus the row of g2 = g - devs
-    const int bi = fin[c] ? boff - (g - b.opt_devs[bo]) * (L + 1) : 0;
+    const unsigned boff = bw3[c] / (256u * CPL);
     // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
     const int bkk = fin[c] ? (int)__ldg(Kg + (size_t)boff * CW + c) : 0;
     const int cand = cand0 + c;
-    if (cand < b.n_cand) {
-      if (k == 1 && g == G) {
-        b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
-        if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
-      }
-      if (fin[c]) {
-        const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
-        if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
-        if (b.full.bp_o) {
-          if (b.full.F) b.full.F[e] = best;
-          if (b.full.N) b.full.N[e] = (double)bkk;
-          b.full.bp_i[e] = bi;
-          b.full.bp_o[e] = bo;
-        }
+    if (top && cand < b.n_cand) {
+      b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
+      if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
+    }
+    if (want_bp && fin[c] && cand < b.n_cand) {
+      const int bo = (int)(bw2[c] & 2047u);
+      // split i of the winner: its successor offset minus the row of g2 = g - devs
+      const int bi = (int)boff - (g - b.opt_devs[bo]) * (L + 1);
+      const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
+      if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
+      if (b.full.bp_o) {
+        if (b.full.F) b.full.F[e] = best;
+        if (b.full.N) b.full.N[e] = (double)bkk;
+        b.full.bp_i[e] = bi;
+        b.full.bp_o[e] = bo;
       }
     }
     // successor entry (state g, split i = k-1) for layer s+1:

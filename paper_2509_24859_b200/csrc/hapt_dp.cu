@@ -58,9 +58,12 @@ int cpl_for(const hapt_tables *t, int n_cand) {
 #ifndef HAPT_U4
 #define HAPT_U4 2
 #endif
+#ifndef HAPT_U2
+#define HAPT_U2 4  // 4 or 8 (a 32-entry stage must be a multiple)
+#endif
 template <int CPL>
 struct Unroll {
-  static constexpr int value = CPL >= 4 ? HAPT_U4 : 4;  // successor loads in flight per warp
+  static constexpr int value = CPL >= 4 ? HAPT_U4 : HAPT_U2;  // successor loads in flight per warp
 };
 
 struct Batch {
@@ -94,6 +97,8 @@ struct Batch {
   int32_t *goff;       // [n_groups+1] exclusive prefix of gtot: the compact cell
                        // index space dp_relax_compact walks
   unsigned *ticket;    // dp_window's last-block counter (self-resetting)
+  int4 *gmeta;         // [G+1] per state g: first option of its mesh, option count,
+                       // available devices, successor boundary row (g_crow)
   uint32_t *spart;     // [kParts][n_groups*cw] finite-cell counts of windowed
                        // layers, spread over kParts copies (dp_states_reduce)
   int n_opts;
@@ -105,7 +110,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], maxlen, clist, gtot, goff, ticket, spart, H0,
+  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], maxlen, clist, gtot, goff, ticket, gmeta, spart, H0,
       H1, K0, K1, total;
 };
 
@@ -129,6 +134,7 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   w.gtot = cur; cur += align_up(ng * 4);
   w.goff = cur; cur += align_up((ng + 1) * 4);
   w.ticket = cur; cur += align_up(4);
+  w.gmeta = cur; cur += align_up((t->G + 1) * sizeof(int4));
   w.spart = cur; cur += align_up(kParts * np * 4);
   w.H0 = cur; cur += align_up(ng * hg * cw * 8);
   w.H1 = cur; cur += align_up(ng * hg * cw * 8);
@@ -171,6 +177,12 @@ __global__ void dp_prep(Batch b) {
     b.irange[1][(size_t)group * (b.G + 1) + g] = empty;
     b.irange[2][(size_t)group * (b.G + 1) + g] = empty;
   }
+  if (group == 0)
+    for (int g = threadIdx.x; g <= b.G; g += blockDim.x) {
+      const int r = b.g_mesh[g];
+      b.gmeta[g] = make_int4(b.opt_off[r], b.opt_off[r + 1] - b.opt_off[r], b.g_avail[g],
+                             b.g_crow[g]);
+    }
   for (int x = threadIdx.x; x < kParts * cw; x += blockDim.x)
     b.spart[(size_t)(x / cw) * b.n_groups * cw + (size_t)group * cw + x % cw] = 0u;
   if (threadIdx.x < cw) {
@@ -415,8 +427,8 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
 #pragma unroll
   for (int c = 0; c < CPL; ++c) cnt2[c] = (unsigned)b.tcnt[cand0 + c] << 11;
   const int imax = L - s + 1;
-  const int r = b.g_mesh[g];
-  const int o0 = b.opt_off[r], nopt = b.opt_off[r + 1] - o0;
+  const int4 gm = b.gmeta[g];
+  const int o0 = gm.x, nopt = gm.y, avail = gm.z;
   const size_t gbase = (size_t)group * b.hg;
   const double *Hg = b.H[(s - 1) & 1] + gbase * CW + lane * CPL;
   const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * CW + lane * CPL;
@@ -440,7 +452,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     if (lane < nch) {
       const int o = o0 + c0 + lane;
       const int devs = b.opt_devs[o], g2 = g - devs;
-      if (devs <= b.g_avail[g] && g2 >= s - 1) {
+      if (devs <= avail && g2 >= s - 1) {
         const int row = o * (L + 2) + k;
         // admissible splits: i <= L-s+1 (later successors are provably
         // infinite), inside the range where state g2's successor entry is
@@ -510,7 +522,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   // epilogue per candidate
   double hn[CPL];
   int kn[CPL];
-  const int crow = b.g_crow[g];
+  const int crow = gm.w;
   const double c2 = crow >= 0 ? __dmul_rn(2.0, b.cb[(size_t)crow * (L + 1) + (k - 1)]) : 0.0;
   const uint8_t *kcp = b.kc + ((size_t)group * b.cb_rows + (crow >= 0 ? crow : 0)) * (L + 1) * CW +
                        (size_t)(k - 1) * CW + lane * CPL;
@@ -892,6 +904,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.goff = (int32_t *)(wb + w.goff);
   b.ticket = (unsigned *)(wb + w.ticket);
   b.spart = (uint32_t *)(wb + w.spart);
+  b.gmeta = (int4 *)(wb + w.gmeta);
   b.n_opts = t->n_opts;
   b.H[0] = (double *)(wb + w.H0);
   b.H[1] = (double *)(wb + w.H1);

@@ -558,6 +558,22 @@ def per_config(args, torch, device) -> dict:
                 "all_ok": bool(((st == 0).all() & (status == 0).all()).item()),
                 "dag_ops_per_s": nodes_edges / dt,
                 "step": "adaptive launch counts + makespan per plan, B=128, inputs in HBM"}
+    # full schedule reports (analyze + steady rate) of 100k plans
+    na = 100_000
+    fa, ba, ca, Sa = config_e(na, seed=7)
+    pa = PlanBatch(fa, ba, ca, stage_counts=Sa, device=device)
+    ca_counts, _ = pa.counts(0.05, "adaptive")
+    pa.analyze(ca_counts, 128)
+    torch.cuda.synchronize()
+    s.record()
+    rep = pa.analyze(ca_counts, 128)
+    e.record()
+    e.synchronize()
+    da = s.elapsed_time(e) * 1e-3
+    out["E_analyze"] = {"plans": na, "plans_per_s": na / da, "seconds": da,
+                        "all_ok": bool((rep.status == 0).all().item()),
+                        "step": "simulate with node times + analyze + steady_state_rate per "
+                                "plan, B=128 (reference: simulate+analyze per plan in Python)"}
     return out
 
 

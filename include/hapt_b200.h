@@ -255,6 +255,28 @@ int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const double *t_fwd
                   double *node_end, const int64_t *node_off, int32_t ring_depth,
                   int32_t *status, void *work, size_t work_bytes, void *stream);
 
+/* Schedule reports of many traces: simulation.analyze(trace, mem_act) and
+ * steady_state_rate(trace, stage=1) (simulation.py:310-395), from the node
+ * times hapt_sim_1f1b wrote at node_off.  Per packed stage x of plan p
+ * (stage s = x - stage_off[p]):
+ *   stage_rep[6x .. 6x+5] = busy, window, bubble, bubble_fraction,
+ *                           steady_bubble, peak_inflight_bytes
+ *   peak_inflight[x]
+ *   link_rep[3x .. 3x+2]  = fwd_time, bwd_time, overlap_ratio of boundary s
+ *                           (NaN for the last stage)
+ * steady_rate[p] = NaN where the reference raises SimulationError (fewer than
+ * 4 aligned samples).  mem_act [total_stages] may be NULL (bytes 0).  status
+ * (nullable) marks plans whose simulation failed: their rows are NaN / -1.
+ * Every figure equals the reference's float bit for bit (CPython's
+ * compensated sum() reproduced). */
+int hapt_analyze_1f1b(int32_t n_plans, int32_t total_stages, const int32_t *stage_off,
+                      const double *t_fwd, const double *t_bwd, const double *comm,
+                      const int32_t *counts, const int32_t *num_mb, const double *mem_act,
+                      const double *node_start, const double *node_end,
+                      const int64_t *node_off, const int32_t *status, double *stage_rep,
+                      int32_t *peak_inflight, double *link_rep, double *steady_rate,
+                      void *stream);
+
 /* Longest-path start times of an arbitrary DAG given as successor CSR:
  * start[v] = max_u (start[u] + duration[u]). processed [1] = number of nodes
  * reached (< n_nodes <=> cycle). */

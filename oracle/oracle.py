@@ -408,6 +408,99 @@ def simulate(t_fwd, t_bwd, comm, counts, B: int):
     return float(mk[0]), start, end
 
 
+def _merge_busy(iv):
+    """Disjoint busy intervals of a set of (lo, hi) (simulation.py:236-246):
+    sort, drop empty ones, fuse overlapping or touching ones."""
+    busy = []
+    for lo, hi in sorted(iv):
+        if not hi > lo:
+            continue
+        if busy and lo <= busy[-1][1]:
+            busy[-1][1] = hi if hi > busy[-1][1] else busy[-1][1]
+        else:
+            busy.append([lo, hi])
+    return [tuple(x) for x in busy]
+
+
+def _overlap(a, b):
+    """Pairwise intersection of two sorted disjoint lists (simulation.py:249-262)."""
+    out, i, j = [], 0, 0
+    while i < len(a) and j < len(b):
+        lo, hi = max(a[i][0], b[j][0]), min(a[i][1], b[j][1])
+        if hi > lo:
+            out.append((lo, hi))
+        if a[i][1] <= b[j][1]:
+            i += 1
+        else:
+            j += 1
+    return out
+
+
+def schedule_report(t_fwd, t_bwd, comm, counts, B: int, mem_act=None):
+    """analyze() + steady_state_rate(stage 1) of one plan (simulation.py:
+    310-395), on the oracle's own explicit-DAG trace.  Reductions use the
+    interpreter's builtin sum() on purpose: that IS the reference's
+    arithmetic (compensated on CPython >= 3.12).  Returns (makespan, stage
+    rows [busy, window, bubble, bubble_fraction, steady_bubble, peak_bytes,
+    peak], link rows [fwd, bwd, overlap], rate or None)."""
+    S = len(t_fwd)
+    mk, start, end = simulate(t_fwd, t_bwd, comm, counts, B)
+    # plain floats: builtin sum() compensates only exact float items
+    start, end = start.tolist(), end.tolist()
+
+    def fb(kind, mb, s):  # reference node numbering (simulation.py:103-111)
+        return 2 * ((s - 1) * B + (mb - 1)) + kind
+
+    def cfb(kind, mb, s):
+        return 2 * S * B + 2 * ((s - 1) * B + (mb - 1)) + kind
+
+    def program(n):  # scheduling.py:241-249
+        ops = [(0, j) for j in range(1, n + 1)]
+        for j in range(1, B - n + 1):
+            ops += [(1, j), (0, n + j)]
+        return ops + [(1, j) for j in range(B - n + 1, B + 1)]
+
+    stages, busy_sets = [], []
+    for s in range(1, S + 1):
+        n = counts[s - 1]
+        ops = program(n)
+        ids = [fb(k, mb, s) for k, mb in ops]
+        dur = [t_fwd[s - 1] if k == 0 else t_bwd[s - 1] for k, _ in ops]
+        busy_sets.append(_merge_busy([(start[v], end[v]) for v in ids]))
+        busy = sum(dur)
+        window = end[ids[-1]] - start[ids[0]]
+        w0, w1 = n, n + 2 * (B - n)
+        sb = ((end[ids[w1 - 1]] - start[ids[w0]]) - sum(dur[w0:w1])) if w1 > w0 else 0.0
+        level, peak = 0, 0
+        for k, _ in ops:
+            level += 1 if k == 0 else -1
+            peak = max(peak, level)
+        per = mem_act[s - 1] if mem_act else 0.0
+        stages.append([busy, window, window - busy,
+                       (window - busy) / window if window > 0 else 0.0, sb, peak * per, peak])
+    links = []
+    for s in range(1, S):
+        ids = [cfb(k, mb, s) for mb in range(1, B + 1) for k in (0, 1)]
+        u = _merge_busy([(start[v], end[v]) for v in ids])
+        tot = sum(hi - lo for lo, hi in u)
+        if tot <= 0.0:
+            ratio = 1.0
+        else:
+            both = _overlap(_overlap(u, busy_sets[s - 1]), busy_sets[s])
+            ratio = sum(hi - lo for lo, hi in both) / tot
+        links.append([sum([comm[s - 1]] * B), sum([comm[s - 1]] * B), ratio])
+    K = counts[0]
+    xs = list(range(2 * K + 1, B + 1, K))
+    rate = None
+    if len(xs) >= 4:
+        ys = [start[fb(0, i, 1)] for i in xs]
+        n = float(len(xs))
+        mx, my = sum(xs) / n, sum(ys) / n
+        rate = (sum((x - mx) * (y - my) for x, y in zip(xs, ys))
+                / sum((x - mx) ** 2 for x in xs))
+    return mk, stages, links, rate
+
+
 def config_e_plans(n_plans: int, seed: int = 24859, B: int = 128):
     """Config E synthetic plan generator: S in {2,3,4,6,8},
     t ~ U(0.5, 2)e-2, f = t*U(.3,.4), b = t - f, bw ~ logU(1, 200) Gbps,

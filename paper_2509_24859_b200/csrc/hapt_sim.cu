@@ -477,6 +477,263 @@ void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const do
       perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status); ::hapt::note_launch();
 }
 
+// ---------------------------------------------------------------------------
+// Schedule analysis (simulation.analyze / steady_state_rate, simulation.py:
+// 310-395) over the node times of many traces.  Every reduction is a CPython
+// builtin sum() over floats -- Neumaier-compensated since 3.12 -- and every
+// interval list is produced in the order the reference's sorted()-based
+// helpers see it, so each figure is the reference's float bit for bit.
+// ---------------------------------------------------------------------------
+
+// sum() of a float sequence: int 0 + first item, then Neumaier (bltinmodule.c)
+struct PySum {
+  double f = 0.0, c = 0.0;
+  bool any = false;
+  __device__ void add(double x) {
+    if (!any) {
+      f = __dadd_rn(0.0, x);
+      any = true;
+      return;
+    }
+    const double t = __dadd_rn(f, x);
+    if (fabs(f) >= fabs(x))
+      c = __dadd_rn(c, __dadd_rn(__dadd_rn(f, -t), x));
+    else
+      c = __dadd_rn(c, __dadd_rn(__dadd_rn(x, -t), f));
+    f = t;
+  }
+  __device__ double value() const {
+    return (c != 0.0 && isfinite(c)) ? __dadd_rn(f, c) : f;
+  }
+};
+
+// One stage's op intervals in program order.  Starts are non-decreasing
+// (start = max(previous end, dependency)), and equal starts only follow a
+// zero-length op, so this is the order sorted() gives _interval_union.
+struct StageSrc {
+  const double *st, *en;
+  int64_t base;  // node id of (F, mb 1) on this stage
+  int N, B, pos;
+  __device__ bool next(double &lo, double &hi) {
+    if (pos >= 2 * B) return false;
+    bool isF;
+    const int mb = decode_op(pos++, N, B, isF);
+    const int64_t id = base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
+    lo = st[id];
+    hi = en[id];
+    return true;
+  }
+};
+
+// One link's transfers: forward (mb order) and backward (mb order) lists are
+// each sorted; merged by (lo, hi) as sorted() orders the concatenation.
+struct LinkSrc {
+  const double *st, *en;
+  int64_t base;  // node id of (CF, mb 1) on this link
+  int B, i, j;   // next forward / backward microbatch (1-based)
+  __device__ bool next(double &lo, double &hi) {
+    const bool hf = i <= B, hb = j <= B;
+    if (!hf && !hb) return false;
+    double flo = 0, fhi = 0, blo = 0, bhi = 0;
+    if (hf) {
+      flo = st[base + 2 * (int64_t)(i - 1)];
+      fhi = en[base + 2 * (int64_t)(i - 1)];
+    }
+    if (hb) {
+      blo = st[base + 2 * (int64_t)(j - 1) + 1];
+      bhi = en[base + 2 * (int64_t)(j - 1) + 1];
+    }
+    if (hf && (!hb || flo < blo || (flo == blo && fhi <= bhi))) {
+      lo = flo, hi = fhi, ++i;
+    } else {
+      lo = blo, hi = bhi, ++j;
+    }
+    return true;
+  }
+};
+
+// _interval_union over a sorted source (empty intervals dropped, touching
+// ones merged)
+template <class Src>
+struct Union {
+  Src src;
+  double clo = 0, chi = 0;
+  bool has = false;
+  __device__ bool next(double &lo, double &hi) {
+    double a, b;
+    while (src.next(a, b)) {
+      if (b <= a) continue;
+      if (!has) {
+        clo = a, chi = b, has = true;
+        continue;
+      }
+      if (a <= chi) {
+        chi = b > chi ? b : chi;
+        continue;
+      }
+      lo = clo, hi = chi;
+      clo = a, chi = b;
+      return true;
+    }
+    if (!has) return false;
+    lo = clo, hi = chi, has = false;
+    return true;
+  }
+};
+
+// _intersect of two sorted disjoint interval streams
+template <class A, class B>
+struct Inter {
+  A a;
+  B b;
+  double alo = 0, ahi = 0, blo = 0, bhi = 0;
+  bool ha = false, hb = false, primed = false;
+  __device__ bool next(double &lo, double &hi) {
+    if (!primed) {
+      ha = a.next(alo, ahi);
+      hb = b.next(blo, bhi);
+      primed = true;
+    }
+    while (ha && hb) {
+      const double l = blo > alo ? blo : alo, h = bhi < ahi ? bhi : ahi;
+      const bool emit = h > l;
+      if (ahi <= bhi)
+        ha = a.next(alo, ahi);
+      else
+        hb = b.next(blo, bhi);
+      if (emit) {
+        lo = l, hi = h;
+        return true;
+      }
+    }
+    return false;
+  }
+};
+
+template <class G>
+__device__ double total_of(G gen) {  // _total: sum(hi - lo)
+  PySum sum;
+  double lo, hi;
+  while (gen.next(lo, hi)) sum.add(__dadd_rn(hi, -lo));
+  return sum.any ? sum.value() : 0.0;
+}
+
+// one thread per stage (and the link behind it): plan p owns stages
+// [stage_off[p], stage_off[p+1])
+__global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t_fwd,
+                          const double *t_bwd, const double *comm, const int32_t *counts,
+                          const int32_t *num_mb, const double *mem_act,
+                          const double *node_start, const double *node_end,
+                          const int64_t *node_off, const int32_t *status, double *stage_rep,
+                          int32_t *peak_inflight, double *link_rep, double *steady_rate) {
+  const int total = stage_off[n_plans];
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= total) return;
+  int lo = 0, hi = n_plans;  // plan p: stage_off[p] <= x < stage_off[p+1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (stage_off[mid] <= x) lo = mid; else hi = mid;
+  }
+  const int p = lo, b0 = stage_off[p], S = stage_off[p + 1] - b0, s = x - b0;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  if (status && status[p] != HAPT_OK) {
+    for (int q = 0; q < 6; ++q) stage_rep[(size_t)x * 6 + q] = nan;
+    for (int q = 0; q < 3; ++q) link_rep[(size_t)x * 3 + q] = nan;
+    peak_inflight[x] = -1;
+    if (s == 0) steady_rate[p] = nan;
+    return;
+  }
+  const int B = num_mb[p], N = counts[x];
+  const int64_t nb = node_off[p];
+  const double *st = node_start, *en = node_end;
+  // -- stage row (simulation.py:331-358) --
+  {
+    StageSrc ops{st, en, nb + 2 * (int64_t)s * B, N, B, 0};
+    PySum busy, steady;
+    int inflight = 0, peak = 0;
+    double first_start = 0, last_end = 0, steady_start = 0, steady_end = 0;
+    const int w0 = N, w1 = N + 2 * (B - N);  // steady ops [w0, w1)
+    for (int q = 0; q < 2 * B; ++q) {
+      bool isF;
+      const int mb = decode_op(q, N, B, isF);
+      const int64_t id = ops.base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
+      const double d = isF ? t_fwd[x] : t_bwd[x];
+      busy.add(d);
+      if (q == 0) first_start = st[id];
+      if (q == 2 * B - 1) last_end = en[id];
+      if (q >= w0 && q < w1) {
+        steady.add(d);
+        if (q == w0) steady_start = st[id];
+        if (q == w1 - 1) steady_end = en[id];
+      }
+      inflight += isF ? 1 : -1;
+      peak = inflight > peak ? inflight : peak;
+    }
+    const double bs = busy.value();
+    const double window = __dadd_rn(last_end, -first_start);
+    const double bubble = __dadd_rn(window, -bs);
+    const double sb = w1 > w0 ? __dadd_rn(__dadd_rn(steady_end, -steady_start), -steady.value())
+                              : 0.0;
+    double *r = stage_rep + (size_t)x * 6;
+    r[0] = bs;
+    r[1] = window;
+    r[2] = bubble;
+    r[3] = window > 0.0 ? __ddiv_rn(bubble, window) : 0.0;
+    r[4] = sb;
+    r[5] = __dmul_rn((double)peak, mem_act ? mem_act[x] : 0.0);
+    peak_inflight[x] = peak;
+  }
+  // -- link row for boundary s (simulation.py:360-378) --
+  double *lr = link_rep + (size_t)x * 3;
+  if (s < S - 1) {
+    const double c = comm[x];
+    PySum f;
+    for (int q = 0; q < B; ++q) f.add(c);
+    const double ft = f.value();
+    const int64_t lbase = nb + 2 * (int64_t)S * B + 2 * (int64_t)s * B;
+    Union<LinkSrc> link{LinkSrc{st, en, lbase, B, 1, 1}};
+    const double tot = total_of(link);
+    double ratio = 1.0;
+    if (tot > 0.0) {
+      Union<StageSrc> u0{StageSrc{st, en, nb + 2 * (int64_t)s * B, N, B, 0}};
+      Union<StageSrc> u1{StageSrc{st, en, nb + 2 * (int64_t)(s + 1) * B, counts[x + 1], B, 0}};
+      Inter<Inter<Union<LinkSrc>, Union<StageSrc>>, Union<StageSrc>> both{
+          Inter<Union<LinkSrc>, Union<StageSrc>>{Union<LinkSrc>{LinkSrc{st, en, lbase, B, 1, 1}},
+                                                 u0},
+          u1};
+      ratio = __ddiv_rn(total_of(both), tot);
+    }
+    lr[0] = ft;
+    lr[1] = ft;  // backward transfers carry the same boundary time
+    lr[2] = ratio;
+  } else {
+    lr[0] = lr[1] = lr[2] = nan;
+  }
+  // -- steady_state_rate(trace, stage=1) (simulation.py:374-395) --
+  if (s == 0) {
+    const int K = N;
+    int n = 0;
+    long long sx = 0;
+    for (int i = 2 * K + 1; i <= B; i += K) ++n, sx += i;
+    if (n < 4) {
+      steady_rate[p] = nan;
+    } else {
+      const double fn = (double)n;
+      const double mx = __ddiv_rn((double)sx, fn);
+      PySum sy;
+      for (int i = 2 * K + 1; i <= B; i += K) sy.add(st[nb + 2 * (int64_t)(i - 1)]);
+      const double my = __ddiv_rn(sy.value(), fn);
+      PySum sxx, sxy;
+      for (int i = 2 * K + 1; i <= B; i += K) {
+        const double dx = __dadd_rn((double)i, -mx);
+        sxx.add(__dmul_rn(dx, dx));  // (x - mean_x) ** 2
+        sxy.add(__dmul_rn(dx, __dadd_rn(st[nb + 2 * (int64_t)(i - 1)], -my)));
+      }
+      steady_rate[p] = __ddiv_rn(sxy.value(), sxx.value());
+    }
+  }
+}
+
 }  // namespace
 }  // namespace hapt
 
@@ -617,5 +874,27 @@ extern "C" int hapt_dag_longest_path(int32_t n_nodes, const int32_t *succ_off,
                                                start, end, makespan, processed, (int32_t *)w,
                                                (int32_t *)(w + a), (int32_t *)(w + 2 * a)); ::hapt::note_launch();
   HAPT_LAUNCHED("k_dag");
+  return HAPT_OK;
+}
+
+extern "C" int hapt_analyze_1f1b(int32_t n_plans, int32_t total_stages, const int32_t *stage_off,
+                                 const double *t_fwd, const double *t_bwd, const double *comm,
+                                 const int32_t *counts, const int32_t *num_mb,
+                                 const double *mem_act, const double *node_start,
+                                 const double *node_end, const int64_t *node_off,
+                                 const int32_t *status, double *stage_rep,
+                                 int32_t *peak_inflight, double *link_rep, double *steady_rate,
+                                 void *stream) {
+  if (n_plans < 1 || total_stages < 1 || !stage_off || !t_fwd || !t_bwd || !comm || !counts ||
+      !num_mb || !node_start || !node_end || !node_off || !stage_rep || !peak_inflight ||
+      !link_rep || !steady_rate) {
+    set_error("hapt_analyze_1f1b: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  k_analyze<<<grid_for(total_stages, 128), 128, 0, (cudaStream_t)stream>>>(
+      n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb, mem_act, node_start, node_end,
+      node_off, status, stage_rep, peak_inflight, link_rep, steady_rate);
+  ::hapt::note_launch();
+  HAPT_LAUNCHED("k_analyze");
   return HAPT_OK;
 }

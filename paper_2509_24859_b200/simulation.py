@@ -362,6 +362,7 @@ class PlanBatch:
             self.t_fwd, self.t_bwd, self.comm = (x[mask].contiguous() for x in (tf, tb, cm))
             self.max_stages = int(sc.max().item())
         self.total_stages = int(self.t_fwd.numel())
+        self.stage_off_host = self.stage_off.cpu().numpy().astype(np.int64)
 
     def counts(self, epsilon: float = 0.05, kind: str = "adaptive", tmax=None):
         """Packed launch counts (hapt_launch_counts) and per-plan status."""
@@ -405,6 +406,117 @@ class PlanBatch:
                                 status.data_ptr(), ws.data_ptr(), nb, stream_ptr()))
         return mk, status
 
+    def analyze(self, counts, num_microbatches, mem_act=None,
+                max_node_bytes: int = 2 << 30) -> "BatchReport":
+        """simulate + analyze + steady_state_rate(stage=1) of every plan
+        (SURVEY.md §8(f)2): per plan the reference's SimulationReport, as
+        packed device arrays.  Plans are processed in chunks whose traces
+        (16 B per DAG node: start and end) fit `max_node_bytes`; each chunk is
+        one hapt_sim_1f1b launch writing node times and one hapt_analyze_1f1b
+        launch reading them back."""
+        import torch
+
+        from . import _lib
+        from ._lib import check, ptr, stream_ptr
+
+        lib = _lib.lib()
+        dev = self.device
+        P, TS = self.n_plans, self.total_stages
+        mb = torch.as_tensor(num_microbatches, dtype=torch.int32).to(dev).reshape(-1)
+        if mb.numel() == 1 and P > 1:
+            mb = mb.expand(P).contiguous()
+        mb_host = mb.cpu().numpy().astype(np.int64)
+        counts = torch.as_tensor(counts, dtype=torch.int32).to(dev).reshape(-1).contiguous()
+        if counts.numel() != TS:
+            raise SimulationError("counts must hold one launch count per packed stage")
+        mem = None
+        if mem_act is not None:
+            mem = torch.as_tensor(mem_act, dtype=torch.float64).to(dev).reshape(-1).contiguous()
+            if mem.numel() != TS:
+                raise SimulationError("mem_act must hold one value per packed stage")
+        so = self.stage_off_host
+        sc = np.diff(so)
+        nodes = mb_host * (4 * sc - 2) + 1  # B(4S-2)+1 per plan (simulation.py:103-111)
+        rep = BatchReport(
+            stage_off=self.stage_off,
+            makespan=torch.empty(P, dtype=torch.float64, device=dev),
+            status=torch.empty(P, dtype=torch.int32, device=dev),
+            stage=torch.empty(TS, 6, dtype=torch.float64, device=dev),
+            peak_inflight=torch.empty(TS, dtype=torch.int32, device=dev),
+            link=torch.empty(TS, 3, dtype=torch.float64, device=dev),
+            steady_rate=torch.empty(P, dtype=torch.float64, device=dev))
+        ring = int(counts.max().item()) + 2
+        cap = max(1, int(max_node_bytes) // 16)
+        p0 = 0
+        while p0 < P:
+            p1, n = p0, 0
+            while p1 < P and (p1 == p0 or n + nodes[p1] <= cap):
+                n += int(nodes[p1])
+                p1 += 1
+            s0, s1 = int(so[p0]), int(so[p1])
+            off = (self.stage_off[p0:p1 + 1] - s0).contiguous()
+            noff = torch.zeros(p1 - p0, dtype=torch.int64, device=dev)
+            if p1 - p0 > 1:
+                noff[1:] = torch.from_numpy(np.cumsum(nodes[p0:p1 - 1])).to(dev)
+            start = torch.empty(n, dtype=torch.float64, device=dev)
+            end = torch.empty(n, dtype=torch.float64, device=dev)
+            nb = lib.hapt_sim_workspace_bytes(s1 - s0, ring)
+            ws = _sim_ws(dev, nb)
+            sl = lambda t: t[s0:s1]  # noqa: E731
+            check(lib.hapt_sim_1f1b(
+                p1 - p0, off.data_ptr(), ptr(sl(self.t_fwd)), ptr(sl(self.t_bwd)),
+                ptr(sl(self.comm)), ptr(sl(counts)), ptr(mb[p0:p1]), ptr(rep.makespan[p0:p1]),
+                start.data_ptr(), end.data_ptr(), noff.data_ptr(), ring,
+                ptr(rep.status[p0:p1]), ws.data_ptr(), nb, stream_ptr()))
+            check(lib.hapt_analyze_1f1b(
+                p1 - p0, s1 - s0, off.data_ptr(), ptr(sl(self.t_fwd)), ptr(sl(self.t_bwd)),
+                ptr(sl(self.comm)), ptr(sl(counts)), ptr(mb[p0:p1]),
+                0 if mem is None else ptr(sl(mem)), start.data_ptr(), end.data_ptr(),
+                noff.data_ptr(), ptr(rep.status[p0:p1]), ptr(rep.stage[s0:s1]),
+                ptr(rep.peak_inflight[s0:s1]), ptr(rep.link[s0:s1]),
+                ptr(rep.steady_rate[p0:p1]), stream_ptr()))
+            p0 = p1
+        return rep
+
+
+@dataclass
+class BatchReport:
+    """Packed per-plan schedule reports (device tensors).  Plan p owns rows
+    [stage_off[p], stage_off[p+1]) of `stage` (busy, window, bubble,
+    bubble_fraction, steady_bubble, peak_inflight_bytes), `peak_inflight`
+    and `link` (fwd_time, bwd_time, overlap_ratio of the boundary after the
+    stage; NaN on the last stage).  steady_rate[p] is steady_state_rate(trace,
+    1), NaN where the reference raises.  status[p] != 0: simulation failed."""
+
+    stage_off: object
+    makespan: object
+    status: object
+    stage: object
+    peak_inflight: object
+    link: object
+    steady_rate: object
+
+    def report(self, p: int) -> "SimulationReport":
+        """Plan p as the reference's SimulationReport (analyze() output)."""
+        a, b = int(self.stage_off[p]), int(self.stage_off[p + 1])
+        if int(self.status[p]) != 0:
+            raise SimulationError(f"plan {p}: simulation failed (status {int(self.status[p])})")
+        st = self.stage[a:b].cpu().numpy()
+        pk = self.peak_inflight[a:b].cpu().numpy()
+        ln = self.link[a:b].cpu().numpy()
+        stages = [StageReport(s + 1, float(st[s, 0]), float(st[s, 1]), float(st[s, 2]),
+                              float(st[s, 3]), float(st[s, 4]), int(pk[s]), float(st[s, 5]))
+                  for s in range(b - a)]
+        links = [LinkReport(s + 1, float(ln[s, 0]), float(ln[s, 1]), float(ln[s, 2]))
+                 for s in range(b - a - 1)]
+        return SimulationReport(float(self.makespan[p]), stages, links)
+
+    def steady_state_rate(self, p: int) -> float:
+        v = float(self.steady_rate[p])
+        if math.isnan(v):
+            raise SimulationError("steady window too short: need >= 3 blocks of microbatches")
+        return v
+
 
 _SIM_WS: dict = {}
 
@@ -430,6 +542,29 @@ def simulate_batch(t_fwd, t_bwd, comm, counts, num_microbatches, stage_counts=No
     as CUDA tensors.
     """
     return _sim_call(t_fwd, t_bwd, comm, counts, num_microbatches, stage_counts=stage_counts)
+
+
+def analyze_batch(t_fwd, t_bwd, comm, counts, num_microbatches, mem_act=None,
+                  stage_counts=None) -> BatchReport:
+    """analyze(simulate(build_dag(...)), mem_act) and steady_state_rate(...,
+    stage=1) of many plans on the device (dense [P, S] inputs as
+    simulate_batch; mem_act [P, S] or None).  BatchReport.report(p) equals the
+    reference's SimulationReport for plan p, float for float."""
+    import torch
+
+    pb = PlanBatch(t_fwd, t_bwd, comm, stage_counts=stage_counts)
+    dev = pb.device
+    cn = torch.as_tensor(counts, dtype=torch.int32).to(dev)
+    mem = None if mem_act is None else torch.as_tensor(mem_act, dtype=torch.float64).to(dev)
+    if stage_counts is None:
+        cn = cn.reshape(-1)
+        mem = None if mem is None else mem.reshape(-1)
+    else:
+        sc = torch.as_tensor(stage_counts, dtype=torch.int32).to(dev)
+        mask = torch.arange(cn.shape[1], device=dev)[None, :] < sc[:, None].long()
+        cn = cn[mask]
+        mem = None if mem is None else mem[mask]
+    return pb.analyze(cn, num_microbatches, mem_act=mem)
 
 
 # ---------------------------------------------------------------------------

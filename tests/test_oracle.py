@@ -114,3 +114,24 @@ def test_config_e_generator_bounds():
         tm = t[p, :s].max()
         assert (c[p, : s - 1] <= tm).all() and (c[p, s - 1 :] == 0).all()
         assert math.isfinite(tm)
+
+
+def test_schedule_report_oracle_equals_reference_goldens():
+    """Oracle restatement of analyze()/steady_state_rate() on its own DAG
+    trace == the reference's reports (tests/golden/analyze.json.gz)."""
+    import gzip
+    import json
+
+    from helpers import GOLDEN
+
+    with gzip.open(GOLDEN + "/analyze.json.gz", "rt") as fh:
+        plans = json.load(fh)
+    for p in plans:
+        mk, stages, links, rate = O.schedule_report(p["t_fwd"], p["t_bwd"], p["comm"],
+                                                    p["counts"], p["B"], p["mem_act"])
+        assert mk.hex() == p["makespan"]
+        for got, want in zip(stages, p["stages"]):
+            assert [float(x).hex() for x in got[:6]] + [got[6]] == want
+        for got, want in zip(links, p["links"]):
+            assert [float(x).hex() for x in got] == want
+        assert (rate is None and p["steady_rate"] is None) or rate.hex() == p["steady_rate"]

@@ -639,3 +639,61 @@ def plan_to_dict(plan: ParallelPlan) -> dict:
         ],
         "search_stats": dict(plan.search_stats),
     }
+
+
+def plan_from_dict(data: dict) -> ParallelPlan:
+    """Inverse of plan_to_dict for plan.yaml files (planner.py:702-747):
+    optional fields default as the reference's, a malformed file raises
+    PlannerError, and a "colocated" boundary carries no transfer time."""
+    def stage(d):
+        lo, hi = d["layers"][0], d["layers"][1]
+        n, m = d["submesh"][0], d["submesh"][1]
+        return PlanStage(int(lo), int(hi), str(d["mesh"]), int(n), int(m), float(d["t_fwd"]),
+                         float(d["t_bwd"]), float(d.get("mem_params", 0.0)),
+                         float(d.get("mem_act", 0.0)), int(d.get("launch_count", 1)),
+                         int(d.get("dp_launch_bound", 1)))
+
+    def boundary(d):
+        link = str(d.get("link", ""))
+        comm = float(d["comm"])  # required even when colocated
+        return PlanBoundary(int(d["after_layer"]), 0.0 if link == "colocated" else comm, link)
+
+    try:
+        stages = [stage(d) for d in data["stages"]]
+        boundaries = [boundary(d) for d in data.get("boundaries", [])]
+    except (KeyError, TypeError, IndexError) as exc:
+        raise PlannerError(f"malformed plan file: {exc}") from exc
+    if len(boundaries) != len(stages) - 1:
+        raise PlannerError("plan needs one boundary per adjacent stage pair")
+    return ParallelPlan(
+        stages=stages, boundaries=boundaries,
+        t_max=float(data.get("t_max", max(s.t for s in stages))),
+        num_microbatches=int(data.get("num_microbatches", 1)),
+        predicted_latency=float(data.get("predicted_latency", 0.0)),
+        eta_pct=float(data.get("eta_pct", 0.0)),
+        epsilon=float(data.get("epsilon", 0.05)),
+        search_stats=dict(data.get("search_stats", {})))
+
+
+_REPORT_STATS = ("backend", "candidates_total", "pruned_below_ts", "pruned_above_te",
+                 "evaluated", "batches", "dp_states")
+
+
+def plan_report(plan: ParallelPlan) -> str:
+    """Human-readable plan summary printed by `meshpipe plan` (planner.py:750-786);
+    same text as the reference."""
+    out = [f"stages: {plan.num_stages}   t_max: {plan.t_max:.6g} s   "
+           f"T*: {plan.predicted_latency:.6g} s (B={plan.num_microbatches})   "
+           f"eta: {plan.eta_pct:.1f}%",
+           "stage  layers      submesh           t/mb        N   K"]
+    for idx, st in enumerate(plan.stages, start=1):
+        head = f"{idx:>5d}  [{st.layer_start:>3d},{st.layer_end:>3d}]  {st.mesh_id}({st.n},{st.m})"
+        out.append(f"{head:<32}{st.t:<10.6g}  {st.launch_count:<3d} {st.dp_launch_bound}")
+    out += [f"  boundary {idx}: after layer {b.after_layer}, {b.comm:.6g} s ({b.link})"
+            for idx, b in enumerate(plan.boundaries, start=1)]
+    stats = plan.search_stats
+    if stats:
+        out.append("search: " + ", ".join(f"{k}={stats[k]}" for k in _REPORT_STATS if k in stats))
+        if "wall_time_s" in stats:
+            out.append(f"wall time: {stats['wall_time_s']:.3f} s")
+    return "\n".join(out) + "\n"

@@ -165,10 +165,10 @@ __global__ void dp_prep(Batch b) {
   __syncthreads();
   double *H = b.H[0] + (size_t)group * b.hg * cw;
   uint16_t *K = b.K[0] + (size_t)group * b.hg * cw;
-  for (size_t x = threadIdx.x; x < b.hg * cw; x += blockDim.x) {
-    H[x] = kInf;
-    K[x] = 0;
-  }
+  // No fill of the successor tables: every read is confined to a state's
+  // finite-successor range (irange), so layer 1 reads only the base entry
+  // (g2 = 0, i = L) written below, and every later entry is written by the
+  // layer before the one that reads it.
   // finite-successor ranges: layer 0 has only (g2 = 0, i = L); the buffers
   // layers 1 and 2 write start empty
   for (int g = threadIdx.x; g <= b.G; g += blockDim.x) {
@@ -237,6 +237,8 @@ __global__ void dp_prep(Batch b) {
     const int row = b.g_crow[0];
     const double c = b.cb[(size_t)row * (b.L + 1) + b.L];
     const size_t e = (size_t)b.L * cw + threadIdx.x;  // g2 = 0, i = L
+    H[e] = kInf;
+    K[e] = 0;
     if (c <= tm) {
       const double c2 = __dmul_rn(2.0, c);
       H[e] = __dadd_rn(c2, 0.0);
@@ -252,10 +254,11 @@ __global__ void dp_prep(Batch b) {
 // k in [lo - maxlen_o + 1, min(hi, L-s+1)].  Cells outside the hull are
 // provably infinite and are never read by layer s+1 (its read range comes
 // from cells that were finite), so dp_relax skips them without writing.
-// Block-wide exclusive scan of one int per thread (blockDim.x == kWinThreads).
-constexpr int kWinThreads = 256;
+// Block-wide exclusive scan of one int per thread (blockDim.x a multiple of
+// 32, at most kWinThreads).
+constexpr int kWinThreads = 1024;
 __device__ __forceinline__ int block_excl_scan(int v, int &total) {
-  __shared__ int wsum[kWinThreads / 32];
+  __shared__ int wsum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int incl = v;
 #pragma unroll
@@ -268,8 +271,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int &total) {
   int before = 0;
   total = 0;
 #pragma unroll
-  for (int w = 0; w < kWinThreads / 32; ++w) {
-    const int x = wsum[w];
+  for (int w = 0; w < 32; ++w) {
+    const int x = w < (int)(blockDim.x >> 5) ? wsum[w] : 0;
     before += w < warp ? x : 0;
     total += x;
   }
@@ -286,21 +289,37 @@ __global__ void __launch_bounds__(kWinThreads) dp_window(Batch b, int s) {
   const int group = blockIdx.x;
   const int L = b.L, G = b.G, imax = L - s + 1;
   int carry = 0;
-  for (int g0 = 0; g0 <= G; g0 += kWinThreads) {
+  for (int g0 = 0; g0 <= G; g0 += blockDim.x) {
     const int g = g0 + threadIdx.x;
     int klo = 0x7fff, khi = 0;
     if (g <= G && g >= s) {
       const int r = b.g_mesh[g], avail = b.g_avail[g];
-      for (int o = b.opt_off[r]; o < b.opt_off[r + 1]; ++o) {
-        const int devs = b.opt_devs[o], g2 = g - devs;
-        if (devs > avail || g2 < s - 1) continue;
-        const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
-        const int hi = min(imax, fr.y);
-        if (fr.x > hi) continue;
-        const int ml = b.maxlen[(size_t)group * b.n_opts + o];
-        if (ml == 0) continue;
-        klo = min(klo, max(1, fr.x - ml + 1));
-        khi = max(khi, hi);
+      const int oa = b.opt_off[r], ob = b.opt_off[r + 1];
+      // four options at a time with independent loads (the per-thread chain
+      // of dependent loads is this kernel's whole cost)
+      for (int o0 = oa; o0 < ob; o0 += 4) {
+        int2 fr[4];
+        int ml[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int o = o0 + u;
+          fr[u] = make_int2(1, 0);
+          ml[u] = 0;
+          if (o < ob) {
+            const int devs = b.opt_devs[o], g2 = g - devs;
+            if (devs <= avail && g2 >= s - 1) {
+              fr[u] = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
+              ml[u] = b.maxlen[(size_t)group * b.n_opts + o];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int hi = min(imax, fr[u].y);
+          if (fr[u].x > hi || ml[u] == 0) continue;
+          klo = min(klo, max(1, fr[u].x - ml[u] + 1));
+          khi = max(khi, hi);
+        }
       }
     }
     const int n = khi >= klo ? khi - klo + 1 : 0;
@@ -324,7 +343,7 @@ __global__ void __launch_bounds__(kWinThreads) dp_window(Batch b, int s) {
   // last block: exclusive prefix of the group totals
   __threadfence();
   int base = 0;
-  for (int j0 = 0; j0 < b.n_groups; j0 += kWinThreads) {
+  for (int j0 = 0; j0 < b.n_groups; j0 += blockDim.x) {
     const int j = j0 + threadIdx.x;
     const int v = j < b.n_groups ? __ldcg(b.gtot + j) : 0;
     int tile;
@@ -931,7 +950,9 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     // GPU holds at once; on small grids its launch costs more than it saves
     const int use_window = cells * b.n_groups >= 32768;
     if (use_window) {
-      dp_window<<<b.n_groups, kWinThreads, 0, st>>>(b, s); ::hapt::note_launch();
+      // one thread per state g (G+1 <= 1024 in one pass)
+      const int wt = min(kWinThreads, (b.G + 1 + 31) / 32 * 32);
+      dp_window<<<b.n_groups, wt, 0, st>>>(b, s); ::hapt::note_launch();
       const unsigned cgrid = grid_for((size_t)cells * b.n_groups, kWarps);
       if (b.cpl == 1)
         dp_relax_compact<1><<<cgrid, kWarps * 32, 0, st>>>(b, s);

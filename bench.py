@@ -502,7 +502,7 @@ def per_config(args, torch, device) -> dict:
     """GPU numbers for the other BASELINE configs (not bench lines)."""
     import numpy as np
 
-    from paper_2509_24859_b200.planner import search, sweep_pool
+    from paper_2509_24859_b200.planner import search, search_batches, sweep_pool
     from paper_2509_24859_b200.profiling import boundary_costs, build_store
     from paper_2509_24859_b200.scheduling import launch_counts_batch
     from paper_2509_24859_b200.simulation import PlanBatch
@@ -525,6 +525,20 @@ def per_config(args, torch, device) -> dict:
                      "T*": plan.predicted_latency, "t_max": plan.t_max,
                      "evaluated": plan.search_stats["evaluated"],
                      "pool": plan.search_stats["candidates_total"]}
+        if name == "D1":  # one set of sweeps for many microbatch counts
+            Bs = [8, 16, 32, 64, 128, 256, 512, 1024]
+            search_batches(st, costs, Bs, epsilon=eps)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            search_batches(build_store(layers, cluster, model, imbalance_ratio=rho),
+                           boundary_costs(layers, cluster), Bs, epsilon=eps)
+            fused = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            for b in Bs:
+                search(build_store(layers, cluster, model, imbalance_ratio=rho),
+                       boundary_costs(layers, cluster), b, epsilon=eps)
+            out["D1_batches"] = {"B": Bs, "search_batches_s": fused,
+                                 "separate_searches_s": time.perf_counter() - t0}
         if name in ("D2", "D3"):
             continue  # full pools of 7k / 16k candidates: search only in the default run
         sweep_pool(st, costs, B)

@@ -196,6 +196,7 @@ class SweepResult:
     winner: int           # argmin (T*, index), -1 if none
     bp: torch.Tensor | None = None     # packed backpointers [n][s_max+1][L+2][G+1]
     ntop: np.ndarray | None = None     # N[s,1,G] per candidate [n][s_max+1]
+    ftop: np.ndarray | None = None     # F[s,1,G] per candidate [n][s_max+1] (keep_ftop)
 
 
 _WS_CACHE: dict = {}  # device -> scratch tensor reused by every Sweeper
@@ -286,11 +287,13 @@ class Sweeper:
         )
         return tstar, best_s, winner
 
-    def evaluate(self, tmax_values, num_microbatches: int, keep_bp: bool = False) -> SweepResult:
+    def evaluate(self, tmax_values, num_microbatches: int, keep_bp: bool = False,
+                 keep_ftop: bool = False) -> SweepResult:
         """Sweep + select a batch; one host transfer for all per-candidate
         results.  keep_bp also records packed backpointers for every
         candidate (when they fit BP_BUDGET) so a winner can be walked without
-        a re-sweep (hapt_dp_walk)."""
+        a re-sweep (hapt_dp_walk); keep_ftop also returns F[s,1,G] per
+        candidate, which does not depend on B (rescoring for other B)."""
         tm = np.asarray(tmax_values, dtype=np.float64)
         n = len(tm)
         tmax = torch.from_numpy(tm).to(self.device)
@@ -306,8 +309,16 @@ class Sweeper:
                  winner.to(torch.int64)]
         if ntop is not None:
             parts.append(ntop.to(torch.int64).reshape(-1))
+        n_ntop = 0 if ntop is None else ntop.numel()
+        if keep_ftop:
+            parts.append(ftop.reshape(-1).view(torch.int64))
         host = torch.cat(parts).cpu().numpy()
+        ftop_host = None
+        if keep_ftop:
+            ftop_host = host[3 * n + 1 + n_ntop:].view(np.float64).reshape(n, -1).copy()
+            host = host[:3 * n + 1 + n_ntop]
         return SweepResult(
+            ftop=ftop_host,
             tmax=tm,
             tstar=host[:n].view(np.float64).copy(),
             best_s=host[n : 2 * n].copy(),

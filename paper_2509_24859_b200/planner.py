@@ -231,7 +231,7 @@ class CandidateEvaluator:
     per-candidate results are all-gathered, so all ranks replay identically."""
 
     def __init__(self, tables: DpTables, pool: Sequence[float], num_microbatches: int,
-                 dist=None):
+                 dist=None, keep_ftop: bool = False):
         self.tables = tables
         self.pool = np.asarray(pool, dtype=np.float64)
         self.B = num_microbatches
@@ -244,6 +244,8 @@ class CandidateEvaluator:
         self.evaluated = 0
         self._bp_of: dict = {}     # pool index -> (SweepResult with bp, position)
         self._bp_bytes = 0
+        # F[s,1,G] per candidate (B-independent) for rescoring under other B
+        self.ftop = np.full((n, tables.s_max + 1), np.inf) if keep_ftop else None
 
     def known(self, idx: int) -> bool:
         return self.best_s[idx] != -2
@@ -258,7 +260,10 @@ class CandidateEvaluator:
             sw = self.tables.sweeper
             need = sw.bp_bytes(len(todo))
             keep = self._bp_bytes + need <= sw.BP_BUDGET
-            res = sw.evaluate(self.pool[todo], self.B, keep_bp=keep)
+            res = sw.evaluate(self.pool[todo], self.B, keep_bp=keep,
+                              keep_ftop=self.ftop is not None)
+            if self.ftop is not None:
+                self.ftop[todo] = res.ftop
             self.tstar[todo] = res.tstar
             self.best_s[todo] = res.best_s
             self.states[todo] = res.states
@@ -276,18 +281,21 @@ class CandidateEvaluator:
         self.ensure([idx])
         return self.best_s[idx] >= 0
 
-    def plan(self, idx: int, epsilon: float) -> "ParallelPlan":
-        """ParallelPlan of pool candidate idx: walked from the batch's kept
+    def plan(self, idx: int, epsilon: float, B: Optional[int] = None,
+             best_s: Optional[int] = None, tstar: Optional[float] = None) -> "ParallelPlan":
+        """ParallelPlan of pool candidate idx (scored for this evaluator's B,
+        or for another B with its best_s / T*): walked from the batch's kept
         backpointers when available, else re-derived by hapt_dp_backtrack."""
+        B = self.B if B is None else B
+        bs = int(self.best_s[idx]) if best_s is None else int(best_s)
+        ts = float(self.tstar[idx]) if tstar is None else float(tstar)
         hit = self._bp_of.get(idx)
         if hit is not None:
             res, pos = hit
-            spans = self.tables.sweeper.walk(res, pos, int(self.best_s[idx]))
-            return _build_plan(self.tables, float(self.pool[idx]), int(self.best_s[idx]),
-                               float(self.tstar[idx]), self.B, epsilon, spans=spans,
-                               n_first=int(res.ntop[pos, int(self.best_s[idx])]))
-        return _build_plan(self.tables, float(self.pool[idx]), int(self.best_s[idx]),
-                           float(self.tstar[idx]), self.B, epsilon)
+            spans = self.tables.sweeper.walk(res, pos, bs)
+            return _build_plan(self.tables, float(self.pool[idx]), bs, ts, B, epsilon,
+                               spans=spans, n_first=int(res.ntop[pos, bs]))
+        return _build_plan(self.tables, float(self.pool[idx]), bs, ts, B, epsilon)
 
 
 def _probe_tree(lo: int, hi: int, depth: int, out: set) -> None:
@@ -570,6 +578,89 @@ def sweep_pool(store: ProfileStore, costs: BoundaryCost, num_microbatches: int, 
         order = np.lexsort((ev.pool[feas], ev.tstar[feas]))
         winner = int(feas[order[0]])
     return ev.pool, ev.tstar, ev.best_s, ev.states, winner
+
+
+def _score(ftop: np.ndarray, tmax: np.ndarray, B: int):
+    """_extract_plan's choice of stage count (planner.py:287-296) for many
+    candidates: first s with the strictly smallest F[s,1,G] + (B-1)*t_max
+    over finite F.  Returns (T*, best_s) with best_s = -1 when infeasible."""
+    pen = float(B - 1) * tmax  # (B - 1) * t_max: int times float
+    tot = ftop[:, 1:] + pen[:, None]  # +inf where F is infinite
+    s = np.argmin(tot, axis=1)
+    t = tot[np.arange(len(tot)), s]
+    ok = np.isfinite(t)
+    return np.where(ok, t, np.inf), np.where(ok, s + 1, -1)
+
+
+def search_batches(store: ProfileStore, costs: BoundaryCost, batch_sizes: Sequence[int],
+                   epsilon: float = 0.05, batch_size: Optional[int] = None,
+                   optimized: bool = True) -> dict:
+    """search() for several microbatch counts from one set of DP sweeps
+    (SURVEY.md §8(f)3).  The DP tables F, N (_dp.pyx:48-95) depend on t_max
+    only, so every candidate is swept once and scored for each B afterwards
+    (T_B = min_s F[s,1,G] + (B-1) t_max).  Feasibility is B-independent, so
+    the reference's binary search (planner.py:456-474) is replayed once; each
+    B then keeps its own t_e cut and merge.  Returns {B: plan}; every plan and
+    its search_stats (but wall_time_s, which is the shared total) equal
+    search(store, costs, B, epsilon, batch_size=batch_size, optimized=...)."""
+    began = time.perf_counter()
+    Bs = [int(b) for b in batch_sizes]
+    if not Bs or min(Bs) < 1:
+        raise PlannerError("batch sizes must be positive integers")
+    tables = DpTables(store, costs)
+    pool = candidate_tmax(store)
+    n = len(pool)
+    ev = CandidateEvaluator(tables, pool, Bs[0], keep_ftop=True)
+    if optimized:
+        lo, _, _, probed = bidirectional_prune_replay(ev, Bs[0])
+        t_lo = np.array([pool[lo]])
+        cuts = {}
+        for B in Bs:
+            ts_lo, _ = _score(ev.ftop[[lo]], t_lo, B)
+            cuts[B] = float(ts_lo[0]) / (B - 1) if B > 1 else math.inf
+        t_cut = max(cuts.values())
+        ev.ensure([i for i in range(lo, n) if pool[i] <= t_cut])
+    else:
+        lo, probed, cuts = 0, [], {B: math.inf for B in Bs}
+        ev.ensure(range(n))
+    transitions = tables.transitions_per_sweep()
+    plans = {}
+    for B in Bs:
+        t_e = cuts[B]
+        surviving = [i for i in range(lo, n) if pool[i] <= t_e]
+        idx = np.asarray(surviving, dtype=np.int64)
+        tstar, best_s = _score(ev.ftop[idx], ev.pool[idx], B)
+        cand = [k for k in range(len(idx)) if best_s[k] >= 0]
+        if not cand:
+            raise InfeasiblePlanError(
+                "no stage partition satisfies the memory and overlap constraints")
+        k = min(cand, key=lambda j: (tstar[j], pool[surviving[j]]))
+        plan = ev.plan(surviving[k], epsilon, B=B, best_s=int(best_s[k]), tstar=float(tstar[k]))
+        if optimized:
+            surv_t = [pool[i] for i in surviving]
+            n_batches = _count_batches(surv_t, _activated_pairs(tables, surv_t), batch_size)
+            evaluated_set = set(probed) | set(surviving)
+        else:
+            n_batches, evaluated_set = 1, set(surviving)
+        # states and feasibility do not depend on B
+        states = int(sum(int(ev.states[i]) for i in evaluated_set if ev.best_s[i] >= 0))
+        plan.search_stats.update({
+            "backend": BACKEND,
+            "candidates_total": n,
+            "pruned_below_ts": lo,
+            "pruned_above_te": n - lo - len(surviving),
+            "evaluated": len(surviving),
+            "batches": n_batches,
+            "t_low": pool[lo],
+            "t_high": None if math.isinf(t_e) else float(t_e),
+            "dp_states": states,
+            "dp_transitions": transitions * len(surviving),
+        })
+        plans[B] = plan
+    wall = time.perf_counter() - began
+    for plan in plans.values():
+        plan.search_stats["wall_time_s"] = wall
+    return plans
 
 
 def validate_plan(plan: ParallelPlan, store: ProfileStore, costs: BoundaryCost, cluster) -> list:

@@ -948,7 +948,9 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     const unsigned long long magic = ((1ull << 32) + nk - 1) / nk;  // ceil(2^32 / nk)
     // the window pass pays off once the layer has far more warps than the
     // GPU holds at once; on small grids its launch costs more than it saves
-    const int use_window = cells * b.n_groups >= 32768;
+    static const long win_min = getenv("HAPT_WINDOW_MIN") ? atol(getenv("HAPT_WINDOW_MIN"))
+                                                          : 32768;
+    const int use_window = cells * b.n_groups >= win_min;
     if (use_window) {
       // one thread per state g (G+1 <= 1024 in one pass)
       const int wt = min(kWinThreads, (b.G + 1 + 31) / 32 * 32);

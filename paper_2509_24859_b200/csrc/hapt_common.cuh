@@ -41,6 +41,36 @@ inline int cuda_status(cudaError_t e, const char *what) {
     if (_st != HAPT_OK) return _st;                               \
   } while (0)
 
+// Programmatic dependent launch (sm_90+).  A kernel enqueued with
+// launch_pdl() may be scheduled while its predecessor in the stream drains:
+// it calls pdl_wait() before touching anything earlier work wrote (a no-op
+// when it was launched normally), then pdl_trigger() so its own successor
+// can be scheduled as soon as every block of this grid is resident.  This
+// hides the launch gap of the layer-by-layer kernel chain.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // HAPT_PDL=0 disables (A/B measurements)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, bool on,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = on ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 inline unsigned grid_for(size_t n, unsigned block) {

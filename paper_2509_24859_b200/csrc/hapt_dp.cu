@@ -157,6 +157,8 @@ __device__ __forceinline__ int upper_bound(const double *a, int n, double v) {
 // the layer-0 successor table: F[0, L+1, 0] = 0 (_dp.pyx:41) is the only
 // finite base state.
 __global__ void dp_prep(Batch b) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_gmax;
   const int group = blockIdx.x;
   const int cw = b.cw;
@@ -286,6 +288,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int &total) {
 // last block), and the reset of the irange buffer layer s+1 writes (last read
 // by layer s-1).
 __global__ void __launch_bounds__(kWinThreads) dp_window(Batch b, int s) {
+  pdl_wait();
+  pdl_trigger();
   const int group = blockIdx.x;
   const int L = b.L, G = b.G, imax = L - s + 1;
   int carry = 0;
@@ -601,6 +605,8 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
 template <int CPL>
 __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     dp_relax(Batch b, int s, int group0, unsigned long long nk_magic) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int CW = 32 * CPL;
   __shared__ int fin_cnt[kWarps][CW];
   __shared__ int4 stage_e[kWarps][32];
@@ -658,6 +664,8 @@ __device__ __forceinline__ int find_group(const int32_t *__restrict__ goff, int 
 template <int CPL>
 __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     dp_relax_compact(Batch b, int s) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int CW = 32 * CPL;
   __shared__ int4 stage_e[kWarps][32];
   __shared__ uint16_t stage_k[kWarps][32];
@@ -717,6 +725,8 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
 
 // states[cand] += sum of the kParts partial counters (padding lanes dropped)
 __global__ void dp_states_reduce(Batch b) {
+  pdl_wait();
+  pdl_trigger();
   const int np = b.n_groups * b.cw;
   for (int cand = blockIdx.x * blockDim.x + threadIdx.x; cand < b.n_cand;
        cand += gridDim.x * blockDim.x) {
@@ -728,6 +738,8 @@ __global__ void dp_states_reduce(Batch b) {
 }
 
 __global__ void dp_ftop_init(double *ftop, unsigned long long *states, int n_cand, int s_max) {
+  pdl_wait();
+  pdl_trigger();
   const long x = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (x < (long)n_cand * (s_max + 1)) ftop[x] = kInf;
   if (x < n_cand) states[x] = 0;
@@ -935,11 +947,16 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   return b;
 }
 
+// The sweep is a chain of ~2 launches per layer; every kernel of it is
+// enqueued with programmatic dependent launch (waits for its predecessor on
+// the device, so the launch gap overlaps the previous kernel's tail).
 int run_sweep(const Batch &b, cudaStream_t st) {
-  dp_ftop_init<<<grid_for((size_t)b.n_cand * (b.s_max + 1), 256), 256, 0, st>>>(
-      b.ftop, b.states, b.n_cand, b.s_max); ::hapt::note_launch();
-  dp_prep<<<b.n_groups, 256, 0, st>>>(b); ::hapt::note_launch();  // block >= 128 = max group width
-  HAPT_LAUNCHED("dp_prep");
+  // measured: on tiny tables (config A, L*G ~ 100) the dependent-launch wait
+  // costs more than the gap it hides
+  const bool pdl = pdl_enabled() && (long)b.L * b.G >= 4096;
+  HAPT_CUDA(launch_pdl(dp_ftop_init, grid_for((size_t)b.n_cand * (b.s_max + 1), 256), 256, st, pdl,
+                       b.ftop, b.states, b.n_cand, b.s_max));
+  HAPT_CUDA(launch_pdl(dp_prep, b.n_groups, 256, st, pdl, b));  // block >= 128 = max group width
   for (int s = 1; s <= b.s_max; ++s) {
     const long cells = (long)(b.L - s + 1) * (b.G - s + 1);
     if (cells <= 0) break;
@@ -954,31 +971,28 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     if (use_window) {
       // one thread per state g (G+1 <= 1024 in one pass)
       const int wt = min(kWinThreads, (b.G + 1 + 31) / 32 * 32);
-      dp_window<<<b.n_groups, wt, 0, st>>>(b, s); ::hapt::note_launch();
+      HAPT_CUDA(launch_pdl(dp_window, b.n_groups, wt, st, pdl, b, s));
       const unsigned cgrid = grid_for((size_t)cells * b.n_groups, kWarps);
+      const dim3 blk(kWarps * 32);
       if (b.cpl == 1)
-        dp_relax_compact<1><<<cgrid, kWarps * 32, 0, st>>>(b, s);
+        HAPT_CUDA(launch_pdl(dp_relax_compact<1>, cgrid, blk, st, pdl, b, s));
       else if (b.cpl == 2)
-        dp_relax_compact<2><<<cgrid, kWarps * 32, 0, st>>>(b, s);
+        HAPT_CUDA(launch_pdl(dp_relax_compact<2>, cgrid, blk, st, pdl, b, s));
       else
-        dp_relax_compact<4><<<cgrid, kWarps * 32, 0, st>>>(b, s);
-      ::hapt::note_launch();
+        HAPT_CUDA(launch_pdl(dp_relax_compact<4>, cgrid, blk, st, pdl, b, s));
       continue;
     }
     for (int g0 = 0; g0 < b.n_groups; g0 += 65535) {
-      const int gy = min(65535, b.n_groups - g0);
+      const dim3 grid(gx, min(65535, b.n_groups - g0)), blk(kWarps * 32);
       if (b.cpl == 1)
-        dp_relax<1><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
+        HAPT_CUDA(launch_pdl(dp_relax<1>, grid, blk, st, pdl, b, s, g0, magic));
       else if (b.cpl == 2)
-        dp_relax<2><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
+        HAPT_CUDA(launch_pdl(dp_relax<2>, grid, blk, st, pdl, b, s, g0, magic));
       else
-        dp_relax<4><<<dim3(gx, gy), kWarps * 32, 0, st>>>(b, s, g0, magic);
-      ::hapt::note_launch();
+        HAPT_CUDA(launch_pdl(dp_relax<4>, grid, blk, st, pdl, b, s, g0, magic));
     }
   }
-  dp_states_reduce<<<grid_for(b.n_cand, 256), 256, 0, st>>>(b);
-  ::hapt::note_launch();
-  HAPT_LAUNCHED("dp_relax");
+  HAPT_CUDA(launch_pdl(dp_states_reduce, grid_for(b.n_cand, 256), 256, st, pdl, b));
   return HAPT_OK;
 }
 

@@ -2,6 +2,7 @@
 // roofline denominator of the fp64-issue-bound kernels (K2, K3): B200's FP64
 // vector peak is not part of MEASURED_PEAKS.json, so bench.py measures it.
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include <atomic>
 
@@ -21,6 +22,14 @@ void set_error(const char *fmt, ...) {
 static std::atomic<long long> g_launches{0};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("HAPT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 namespace {
 // 8 independent DADD chains per thread; iters * 8 adds per thread.

@@ -422,7 +422,15 @@ def main():
         },
     }
 
-    # e2e through the public API from host inputs (rank-sharded when N>1)
+    # e2e through the public API from host inputs (rank-sharded when N>1).
+    # Long-lived interpreter objects (torch, numpy, the loaded instance) are
+    # moved out of the cyclic GC's generations first (gc.freeze, the usual
+    # setting for latency-sensitive Python services): otherwise a full
+    # collection of ~25 ms lands in random steps (measured on the box).
+    import gc
+
+    gc.collect()
+    gc.freeze()
     e2e_times = []
     h2d = 8 * (3 * Lr + 4 * len(cluster.meshes)) + 4 * (Lr + 2 * len(cluster.meshes) + 3 * len(store.options))
     for i in range(2 + args.steps):
@@ -473,7 +481,8 @@ def main():
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "path": "build_store -> boundary_costs -> planner.sweep_pool (host in, host out)"},
+                "path": "build_store -> boundary_costs -> planner.sweep_pool (host in, host out)",
+                "host_gc": "gc.freeze() after warm-up"},
         "search_time_s": search_time,
         "search_plan": {"stages": plan.num_stages, "T*": plan.predicted_latency,
                         "t_max": plan.t_max, "evaluated": plan.search_stats["evaluated"]},

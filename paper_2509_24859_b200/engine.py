@@ -13,6 +13,7 @@ copies and sequences calls.
 from __future__ import annotations
 
 import ctypes
+import weakref
 import math
 from dataclasses import dataclass
 
@@ -220,7 +221,10 @@ class Sweeper:
     BP_BUDGET = 6 * 2**30  # bytes of packed backpointers kept for a batch
 
     def __init__(self, tables: DeviceTables, max_ws_bytes: int | None = None):
-        self.tables = tables
+        # weak: DeviceTables caches its Sweeper, and a strong back-reference
+        # would make the pair a cycle that only the cyclic GC frees -- the
+        # 100 MB tables buffer must go back to the allocator by refcount
+        self._tables = weakref.ref(tables)
         self.lib = tables.lib
         self.device = tables.device
         if max_ws_bytes is None:
@@ -230,6 +234,13 @@ class Sweeper:
         self.max_ws_bytes = max_ws_bytes
         self._bt_ws = None
         self.last_chunks = 0
+
+    @property
+    def tables(self) -> "DeviceTables":
+        t = self._tables()
+        if t is None:
+            raise RuntimeError("the device tables of this sweeper were released")
+        return t
 
     def _chunk(self) -> int:
         per32 = self.lib.hapt_dp_workspace_bytes(ctypes.byref(self.tables.t), 32)

@@ -99,6 +99,7 @@ class DeviceTables:
         self._keep = keep  # inputs must outlive the asynchronous build
         self._counters = None
         self._host.clear()
+        self._transitions = None  # planner.DpTables.transitions_per_sweep cache
         return self
 
     def load_dense(self, arrays: dict, s_max: int) -> "DeviceTables":
@@ -131,6 +132,7 @@ class DeviceTables:
         check(self.lib.hapt_tables_finalize(ctypes.byref(self.t), stream_ptr()))
         self._counters = None
         self._host.clear()
+        self._transitions = None  # planner.DpTables.transitions_per_sweep cache
         return self
 
     # -- host-side reads -----------------------------------------------------

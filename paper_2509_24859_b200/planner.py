@@ -201,15 +201,23 @@ class DpTables:
         return self.dev._sweeper
 
     def transitions_per_sweep(self) -> int:
+        """planner.py:250-258: sum over states g of the feasible spans of the
+        options of g's mesh that fit in g's available devices, times s_max
+        (vectorised over states; cached per tables)."""
+        cached = getattr(self.dev, "_transitions", None)
+        if cached is not None and cached[0] == self.s_max:
+            return cached[1]
         per_opt = self.feasible_spans_per_opt
-        g_mesh, g_avail = self.g_mesh, self.g_avail
+        g_mesh, g_avail = self.g_mesh[1:].astype(np.int64), self.g_avail[1:].astype(np.int64)
         off, devs = self.opt_off, self.opt_devs
         total = 0
-        for g in range(1, self.G + 1):
-            r = int(g_mesh[g])
-            for o in range(int(off[r]), int(off[r + 1])):
-                if devs[o] <= g_avail[g]:
-                    total += int(per_opt[o])
+        for r in range(len(off) - 1):
+            o = np.arange(int(off[r]), int(off[r + 1]))
+            avail = g_avail[g_mesh == r]
+            if len(o) and len(avail):
+                fits = devs[o][None, :] <= avail[:, None]
+                total += int((fits * per_opt[o][None, :]).sum())
+        self.dev._transitions = (self.s_max, total * self.s_max)
         return total * self.s_max
 
 

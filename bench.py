@@ -548,6 +548,24 @@ def per_config(args, torch, device) -> dict:
                        boundary_costs(layers, cluster), b, epsilon=eps)
             out["D1_batches"] = {"B": Bs, "search_batches_s": fused,
                                  "separate_searches_s": time.perf_counter() - t0}
+            # config D's full microbatch-config sweep: operator graph
+            # -> front end -> store -> search for (mb, B) in (1,128)..(8,16)
+            from paper_2509_24859_b200.sweep import best_point, microbatch_sweep
+            from paper_2509_24859_b200.workloads import llama_like_ops
+
+            microbatch_sweep(lambda mb: llama_like_ops(b=mb), cluster, model=model,
+                             imbalance_ratio=rho, epsilon=eps)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pts = microbatch_sweep(lambda mb: llama_like_ops(b=mb), cluster, model=model,
+                                   imbalance_ratio=rho, epsilon=eps)
+            bp = best_point(pts)
+            out["D_microbatch_sweep"] = {
+                "points": [[p.mb_size, p.num_microbatches, p.plan.predicted_latency]
+                           for p in pts],
+                "best": [bp.mb_size, bp.num_microbatches], "seconds": time.perf_counter() - t0,
+                "step": "ops -> detect_modules -> cluster_layers -> build_store -> search, "
+                        "4 points, end to end on host inputs"}
         if name in ("D2", "D3"):
             continue  # full pools of 7k / 16k candidates: search only in the default run
         sweep_pool(st, costs, B)

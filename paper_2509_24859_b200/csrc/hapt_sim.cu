@@ -317,7 +317,8 @@ template <int S>
 __global__ void __launch_bounds__(SimCfg<S>::threads)
     k_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
             const double *t_bwd, const double *comm, const int32_t *counts,
-            const int32_t *num_mb, double *makespan, int32_t *status) {
+            const int32_t *num_mb, double *makespan, int32_t *status, double *node_start,
+            double *node_end, const int64_t *node_off) {
   extern __shared__ double ring[];  // [(S-1) links][2 dirs][kRing][threads]
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -351,6 +352,9 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
     prev[s] = lcf[s] = lcb[s] = 0.0;
   }
   double mk = 0.0;
+  // optional per-node times in the reference numbering (simulation.py:103-111)
+  const bool nodes = node_start != nullptr;
+  const int64_t nb = nodes ? node_off[p] : 0, cf0 = nb + 2 * (int64_t)S * B;
   int remaining = S;
   while (remaining > 0) {
     bool progress = false;
@@ -372,21 +376,38 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
           const double en = __dadd_rn(st, isF ? tf[s] : tb[s]);
           prev[s] = en;
           mk = fmax(mk, en);
+          if (nodes) {
+            const int64_t id = nb + 2 * ((int64_t)s * B + (mb - 1)) + (isF ? 0 : 1);
+            node_start[id] = st;
+            node_end[id] = en;
+          }
           if (isF) {
             fd[s] = mb;
             if (s < S - 1) {  // forward transfer on link s (simulation.py:130-140)
-              const double ce = __dadd_rn(fmax(en, lcf[s]), cm[s]);
+              const double cs = fmax(en, lcf[s]);
+              const double ce = __dadd_rn(cs, cm[s]);
               lcf[s] = ce;
               mk = fmax(mk, ce);
               slot(s, 0, mb) = ce;
+              if (nodes) {
+                const int64_t id = cf0 + 2 * ((int64_t)s * B + (mb - 1));
+                node_start[id] = cs;
+                node_end[id] = ce;
+              }
             }
           } else {
             bd[s] = mb;
             if (s > 0) {  // backward transfer on link s-1
-              const double ce = __dadd_rn(fmax(en, lcb[s - 1]), cm[s - 1]);
+              const double cs = fmax(en, lcb[s - 1]);
+              const double ce = __dadd_rn(cs, cm[s - 1]);
               lcb[s - 1] = ce;
               mk = fmax(mk, ce);
               slot(s - 1, 1, mb) = ce;
+              if (nodes) {
+                const int64_t id = cf0 + 2 * ((int64_t)(s - 1) * B + (mb - 1)) + 1;
+                node_start[id] = cs;
+                node_end[id] = ce;
+              }
             }
           }
           if (++pos[s] == 2 * B) --remaining;
@@ -398,6 +419,11 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
       status[p] = kRetry;  // let the generic kernel decide (deadlock vs. depth)
       return;
     }
+  }
+  if (nodes) {  // the sink
+    const int64_t sink = cf0 + 2 * (int64_t)(S - 1) * B;
+    node_start[sink] = mk;
+    node_end[sink] = mk;
   }
   makespan[p] = mk;
   status[p] = HAPT_OK;
@@ -465,7 +491,8 @@ __global__ void k_sim_retry(int n_plans, const int32_t *status, int32_t *perm, i
 template <int S>
 void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
                   const double *t_bwd, const double *comm, const int32_t *counts,
-                  const int32_t *num_mb, double *makespan, int32_t *status, cudaStream_t st) {
+                  const int32_t *num_mb, double *makespan, int32_t *status, double *node_start,
+                  double *node_end, const int64_t *node_off, cudaStream_t st) {
   if (n <= 0) return;
   using C = SimCfg<S>;
   static bool attr = false;
@@ -474,7 +501,8 @@ void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const do
     attr = true;
   }
   k_sim_s<S><<<grid_for(n, C::threads), C::threads, C::smem, st>>>(
-      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status); ::hapt::note_launch();
+      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, node_start,
+      node_end, node_off); ::hapt::note_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -618,37 +646,49 @@ __device__ double total_of(G gen) {  // _total: sum(hi - lo)
   return sum.any ? sum.value() : 0.0;
 }
 
-// one thread per stage (and the link behind it): plan p owns stages
-// [stage_off[p], stage_off[p+1])
+// Three thread ranges, so that a warp's threads run the same kind of row
+// (a mixed warp serialises a long link walk behind short stage rows):
+//   [0, T)        the stage row of packed stage x
+//   [T, 2T)       the link row behind packed stage x (NaN on a plan's last stage)
+//   [2T, 2T + P)  steady_state_rate of plan p
+// (T = total stages, P = plans; plan p owns stages [stage_off[p], stage_off[p+1])).
 __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t_fwd,
                           const double *t_bwd, const double *comm, const int32_t *counts,
                           const int32_t *num_mb, const double *mem_act,
                           const double *node_start, const double *node_end,
                           const int64_t *node_off, const int32_t *status, double *stage_rep,
                           int32_t *peak_inflight, double *link_rep, double *steady_rate) {
-  const int total = stage_off[n_plans];
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= total) return;
-  int lo = 0, hi = n_plans;  // plan p: stage_off[p] <= x < stage_off[p+1]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (stage_off[mid] <= x) lo = mid; else hi = mid;
+  const long T = stage_off[n_plans];
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int role = t < T ? 0 : t < 2 * T ? 1 : t < 2 * T + n_plans ? 2 : 3;
+  if (role == 3) return;
+  int p, x;
+  if (role == 2) {
+    p = (int)(t - 2 * T);
+    x = stage_off[p];
+  } else {
+    x = (int)(role == 0 ? t : t - T);
+    int lo = 0, hi = n_plans;  // plan p: stage_off[p] <= x < stage_off[p+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (stage_off[mid] <= x) lo = mid; else hi = mid;
+    }
+    p = lo;
   }
-  const int p = lo, b0 = stage_off[p], S = stage_off[p + 1] - b0, s = x - b0;
+  const int b0 = stage_off[p], S = stage_off[p + 1] - b0, s = x - b0;
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
-  if (status && status[p] != HAPT_OK) {
-    for (int q = 0; q < 6; ++q) stage_rep[(size_t)x * 6 + q] = nan;
-    for (int q = 0; q < 3; ++q) link_rep[(size_t)x * 3 + q] = nan;
-    peak_inflight[x] = -1;
-    if (s == 0) steady_rate[p] = nan;
-    return;
-  }
-  const int B = num_mb[p], N = counts[x];
+  const bool failed = status && status[p] != HAPT_OK;
+  const int B = num_mb[p];
   const int64_t nb = node_off[p];
   const double *st = node_start, *en = node_end;
-  // -- stage row (simulation.py:331-358) --
-  {
-    StageSrc ops{st, en, nb + 2 * (int64_t)s * B, N, B, 0};
+  if (role == 0) {  // -- stage row (simulation.py:331-358) --
+    if (failed) {
+      for (int q = 0; q < 6; ++q) stage_rep[(size_t)x * 6 + q] = nan;
+      peak_inflight[x] = -1;
+      return;
+    }
+    const int N = counts[x];
+    const int64_t base = nb + 2 * (int64_t)s * B;
     PySum busy, steady;
     int inflight = 0, peak = 0;
     double first_start = 0, last_end = 0, steady_start = 0, steady_end = 0;
@@ -656,7 +696,7 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     for (int q = 0; q < 2 * B; ++q) {
       bool isF;
       const int mb = decode_op(q, N, B, isF);
-      const int64_t id = ops.base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
+      const int64_t id = base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
       const double d = isF ? t_fwd[x] : t_bwd[x];
       busy.add(d);
       if (q == 0) first_start = st[id];
@@ -682,10 +722,14 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     r[4] = sb;
     r[5] = __dmul_rn((double)peak, mem_act ? mem_act[x] : 0.0);
     peak_inflight[x] = peak;
+    return;
   }
-  // -- link row for boundary s (simulation.py:360-378) --
-  double *lr = link_rep + (size_t)x * 3;
-  if (s < S - 1) {
+  if (role == 1) {  // -- link row for boundary s (simulation.py:360-378) --
+    double *lr = link_rep + (size_t)x * 3;
+    if (failed || s >= S - 1) {
+      lr[0] = lr[1] = lr[2] = nan;
+      return;
+    }
     const double c = comm[x];
     PySum f;
     for (int q = 0; q < B; ++q) f.add(c);
@@ -695,7 +739,7 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     const double tot = total_of(link);
     double ratio = 1.0;
     if (tot > 0.0) {
-      Union<StageSrc> u0{StageSrc{st, en, nb + 2 * (int64_t)s * B, N, B, 0}};
+      Union<StageSrc> u0{StageSrc{st, en, nb + 2 * (int64_t)s * B, counts[x], B, 0}};
       Union<StageSrc> u1{StageSrc{st, en, nb + 2 * (int64_t)(s + 1) * B, counts[x + 1], B, 0}};
       Inter<Inter<Union<LinkSrc>, Union<StageSrc>>, Union<StageSrc>> both{
           Inter<Union<LinkSrc>, Union<StageSrc>>{Union<LinkSrc>{LinkSrc{st, en, lbase, B, 1, 1}},
@@ -706,32 +750,33 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     lr[0] = ft;
     lr[1] = ft;  // backward transfers carry the same boundary time
     lr[2] = ratio;
-  } else {
-    lr[0] = lr[1] = lr[2] = nan;
+    return;
   }
   // -- steady_state_rate(trace, stage=1) (simulation.py:374-395) --
-  if (s == 0) {
-    const int K = N;
-    int n = 0;
-    long long sx = 0;
-    for (int i = 2 * K + 1; i <= B; i += K) ++n, sx += i;
-    if (n < 4) {
-      steady_rate[p] = nan;
-    } else {
-      const double fn = (double)n;
-      const double mx = __ddiv_rn((double)sx, fn);
-      PySum sy;
-      for (int i = 2 * K + 1; i <= B; i += K) sy.add(st[nb + 2 * (int64_t)(i - 1)]);
-      const double my = __ddiv_rn(sy.value(), fn);
-      PySum sxx, sxy;
-      for (int i = 2 * K + 1; i <= B; i += K) {
-        const double dx = __dadd_rn((double)i, -mx);
-        sxx.add(__dmul_rn(dx, dx));  // (x - mean_x) ** 2
-        sxy.add(__dmul_rn(dx, __dadd_rn(st[nb + 2 * (int64_t)(i - 1)], -my)));
-      }
-      steady_rate[p] = __ddiv_rn(sxy.value(), sxx.value());
-    }
+  if (failed) {
+    steady_rate[p] = nan;
+    return;
   }
+  const int K = counts[x];
+  int n = 0;
+  long long sx = 0;
+  for (int i = 2 * K + 1; i <= B; i += K) ++n, sx += i;
+  if (n < 4) {
+    steady_rate[p] = nan;
+    return;
+  }
+  const double fn = (double)n;
+  const double mx = __ddiv_rn((double)sx, fn);
+  PySum sy;
+  for (int i = 2 * K + 1; i <= B; i += K) sy.add(st[nb + 2 * (int64_t)(i - 1)]);
+  const double my = __ddiv_rn(sy.value(), fn);
+  PySum sxx, sxy;
+  for (int i = 2 * K + 1; i <= B; i += K) {
+    const double dx = __dadd_rn((double)i, -mx);
+    sxx.add(__dmul_rn(dx, dx));  // (x - mean_x) ** 2
+    sxy.add(__dmul_rn(dx, __dadd_rn(st[nb + 2 * (int64_t)(i - 1)], -my)));
+  }
+  steady_rate[p] = __ddiv_rn(sxy.value(), sxx.value());
 }
 
 }  // namespace
@@ -793,7 +838,7 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   int32_t *perm = (int32_t *)wt;
   int32_t *cnt = (int32_t *)(wt + align_up((size_t)n_plans * 4));
   int32_t *bhist = cnt + 32;
-  if (node_start) {  // per-node outputs (simulate() on one plan): generic walk
+  if (node_start && n_plans < 4096) {  // per-node outputs of a few plans: generic walk
     k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, nullptr, nullptr, stage_off, t_fwd,
                                                   t_bwd, comm, counts, num_mb, makespan,
                                                   node_start, node_end, node_off, ring_depth,
@@ -828,7 +873,7 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   if (h[SV] > 0) {                                                                            \
     HAPT_CUDA(cudaStreamWaitEvent(side[SV], ev[0], 0));                                       \
     launch_sim_s<SV>(perm + h[10 + SV], h[SV], stage_off, t_fwd, t_bwd, comm, counts, num_mb, \
-                     makespan, status, side[SV]);                                             \
+                     makespan, status, node_start, node_end, node_off, side[SV]);             \
     HAPT_CUDA(cudaEventRecord(ev[SV], side[SV]));                                             \
     HAPT_CUDA(cudaStreamWaitEvent(st, ev[SV], 0));                                            \
   }
@@ -841,14 +886,14 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   HAPT_CUDA(cudaMemsetAsync(cnt + 20, 0, 4, st));
   if (h[0] > 0) {
     k_sim<<<grid_for(h[0], 128), 128, 0, st>>>(h[0], perm, cnt + 0, stage_off, t_fwd, t_bwd,
-                                               comm, counts, num_mb, makespan, nullptr, nullptr,
-                                               nullptr, ring_depth, ring, status);
+                                               comm, counts, num_mb, makespan, node_start,
+                                               node_end, node_off, ring_depth, ring, status);
     ::hapt::note_launch();
   }
   k_sim_retry<<<grid_for(n_plans, 256), 256, 0, st>>>(n_plans, status, perm + h[0], cnt + 20); ::hapt::note_launch();
   k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, perm + h[0], cnt + 20, stage_off,
                                                 t_fwd, t_bwd, comm, counts, num_mb, makespan,
-                                                nullptr, nullptr, nullptr, ring_depth, ring,
+                                                node_start, node_end, node_off, ring_depth, ring,
                                                 status); ::hapt::note_launch();
   HAPT_LAUNCHED("k_sim");
   return HAPT_OK;
@@ -891,7 +936,7 @@ extern "C" int hapt_analyze_1f1b(int32_t n_plans, int32_t total_stages, const in
     set_error("hapt_analyze_1f1b: invalid arguments");
     return HAPT_EINVAL;
   }
-  k_analyze<<<grid_for(total_stages, 128), 128, 0, (cudaStream_t)stream>>>(
+  k_analyze<<<grid_for(2 * (size_t)total_stages + n_plans, 128), 128, 0, (cudaStream_t)stream>>>(
       n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb, mem_act, node_start, node_end,
       node_off, status, stage_rep, peak_inflight, link_rep, steady_rate);
   ::hapt::note_launch();

@@ -130,3 +130,14 @@ def check_against_goldens_subset(rep, plans, idx):
     for i in idx:
         for s, row in enumerate(plans[i]["stages"]):
             assert [float(x).hex() for x in st[so[i] + s]] == row[:6]
+
+
+def test_analyze_large_batch_fast_path():
+    """A batch large enough for the bucketed per-S simulation kernels (which
+    then also write the node times) gives the same reports."""
+    from paper_2509_24859_b200.simulation import analyze_batch
+
+    plans = load() * 11  # 4,400 plans: past the generic-walk threshold
+    tf, tb, cm, cn, B, mem, sc = dense(plans)
+    rep = analyze_batch(tf, tb, cm, cn, B, mem_act=mem, stage_counts=sc)
+    check_against_goldens(rep, plans)

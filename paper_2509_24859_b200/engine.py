@@ -220,7 +220,9 @@ class Sweeper:
     candidate batches are chunked so the successor tables stay within
     `max_ws_bytes`."""
 
-    BP_BUDGET = 6 * 2**30  # bytes of packed backpointers kept for a batch
+    # bytes of packed backpointers kept for a batch: a quarter of the free HBM
+    # at first use, at most 40 GB (a D3 survivor batch needs ~24 GB)
+    BP_CAP = 40 * 2**30
 
     def __init__(self, tables: DeviceTables, max_ws_bytes: int | None = None):
         # weak: DeviceTables caches its Sweeper, and a strong back-reference
@@ -229,11 +231,12 @@ class Sweeper:
         self._tables = weakref.ref(tables)
         self.lib = tables.lib
         self.device = tables.device
+        if self.device not in _FREE_MEM:
+            _FREE_MEM[self.device] = torch.cuda.mem_get_info(self.device)[0]
         if max_ws_bytes is None:
-            if self.device not in _FREE_MEM:
-                _FREE_MEM[self.device] = torch.cuda.mem_get_info(self.device)[0]
             max_ws_bytes = int(min(0.5 * _FREE_MEM[self.device], 48 * 2**30))
         self.max_ws_bytes = max_ws_bytes
+        self.BP_BUDGET = int(min(self.BP_CAP, 0.25 * _FREE_MEM[self.device]))
         self._bt_ws = None
         self.last_chunks = 0
 

@@ -258,7 +258,11 @@ class CandidateEvaluator:
     def known(self, idx: int) -> bool:
         return self.best_s[idx] != -2
 
-    def ensure(self, indices) -> None:
+    def ensure(self, indices, keep_bp: bool = True) -> None:
+        """Evaluate the unknown candidates among `indices` in one batch.
+        keep_bp: record the batch's backpointers (within BP_BUDGET) so a
+        winner from it is walked instead of re-swept -- worth it only for a
+        batch that can contain the final winner."""
         todo = sorted({int(i) for i in indices if not self.known(int(i))})
         if not todo:
             return
@@ -267,7 +271,7 @@ class CandidateEvaluator:
         if self.dist is None:
             sw = self.tables.sweeper
             need = sw.bp_bytes(len(todo))
-            keep = self._bp_bytes + need <= sw.BP_BUDGET
+            keep = keep_bp and self._bp_bytes + need <= sw.BP_BUDGET
             res = sw.evaluate(self.pool[todo], self.B, keep_bp=keep,
                               keep_ftop=self.ftop is not None)
             if self.ftop is not None:
@@ -328,6 +332,9 @@ def _batch_depth(tables: DpTables, pool_len: int) -> int:
     return d
 
 
+_SURVIVOR_SPEC = 1024  # cap on the candidates swept speculatively with the last probes
+
+
 def _full_pool_is_cheap(tables: DpTables, pool_len: int) -> bool:
     cells = max(1, tables.L * tables.G)
     return math.ceil(pool_len / 32) * cells <= 2 * 40_000
@@ -342,20 +349,34 @@ def bidirectional_prune_replay(ev: CandidateEvaluator, num_microbatches: int):
     probed: list[int] = []
     lo, hi = 0, n - 1
     depth = _batch_depth(ev.tables, n)
+
+    def batch(lo: int, hi: int, top: bool) -> None:
+        """The probes the next `depth` steps from (lo, hi) can touch.  If the
+        binary search ends inside them, also the candidates the surviving
+        set t_S <= t <= t_E can reach (t_E estimated from the feasible upper
+        end: T grows with t_max once (B-1) t_max dominates, so this
+        over-covers; a miss only costs a survivor batch), and keep this
+        batch's backpointers for the winner."""
+        spec = {hi} if top else set()
+        _probe_tree(lo, hi, depth, spec)
+        final = (hi - lo + 1).bit_length() <= depth
+        if final and ev.known(hi) and ev.best_s[hi] >= 0:
+            B = num_microbatches
+            t_est = ev.tstar[hi] / (B - 1) if B > 1 else math.inf
+            end = int(np.searchsorted(ev.pool, t_est, side="right")) + 8
+            spec.update(range(lo, min(n, max(hi + 1, end), lo + _SURVIVOR_SPEC)))
+        ev.ensure(spec, keep_bp=final)
+
     if _full_pool_is_cheap(ev.tables, n):
         ev.ensure(range(n))
-    spec = {hi}
-    _probe_tree(lo, hi, depth, spec)
-    ev.ensure(spec)
+    batch(lo, hi, top=True)
     probed.append(hi)
     if not ev.feasible(hi):
         raise InfeasiblePlanError("no t_max candidate admits a feasible plan")
     while lo < hi:
         mid = (lo + hi) // 2
         if not ev.known(mid):
-            spec = set()
-            _probe_tree(lo, hi, depth, spec)
-            ev.ensure(spec)
+            batch(lo, hi, top=False)
         probed.append(mid)
         if ev.feasible(mid):
             hi = mid
@@ -579,7 +600,7 @@ def sweep_pool(store: ProfileStore, costs: BoundaryCost, num_microbatches: int, 
     tables = DpTables(store, costs)
     pool = candidate_tmax(store)
     ev = CandidateEvaluator(tables, pool, num_microbatches, dist)
-    ev.ensure(range(len(pool)))
+    ev.ensure(range(len(pool)), keep_bp=False)  # no plan is built from a pool sweep
     feas = np.where(ev.best_s >= 0)[0]
     winner = -1
     if len(feas):

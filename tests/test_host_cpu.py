@@ -43,7 +43,7 @@ class FakeEvaluator:
     def known(self, i):
         return self.best_s[i] != -2
 
-    def ensure(self, idx):
+    def ensure(self, idx, keep_bp=True):
         todo = [i for i in idx if not self.known(i)]
         if todo:
             self.batches.append(sorted(todo))

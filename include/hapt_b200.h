@@ -206,6 +206,16 @@ int hapt_dp_select(const double *ftop, const double *tmax, int32_t n_cand,
                    int32_t s_max, int64_t num_microbatches, double *tstar,
                    int32_t *best_s, int32_t *winner, void *stream);
 
+/* The reference operator itself, one t_max: replaces _core.dp_sweep
+ * (_dp.pyx:14-97) for a caller that keeps the reference's one-candidate loop.
+ * F, N (fp64) and bp_i, bp_o (int32) are device arrays [s_max+1][L+2][G+1]
+ * in the reference layout; the library writes every element (F = +inf but
+ * F[0,L+1,0] = 0, N = 0, bp = -1, then the DP), so they need no pre-fill.
+ * t_max <= 0 is HAPT_EINVAL (planner.py:396-397 raises). */
+size_t hapt_dp_sweep_workspace_bytes(const hapt_tables *t);
+int hapt_dp_sweep(const hapt_tables *t, double t_max, double *F, double *N, int32_t *bp_i,
+                  int32_t *bp_o, void *work, size_t work_bytes, void *stream);
+
 /* Re-sweep one candidate with backpointers and walk the chain from
  * (best_s, 1, G). stages [s_max][3] = (layer_start, layer_end, option);
  * kchain [s_max] = DP launch bounds K; n_stages [1]. */

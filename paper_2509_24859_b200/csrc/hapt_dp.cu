@@ -1108,6 +1108,55 @@ extern "C" int hapt_dp_backtrack(const hapt_tables *t, double tmax, int32_t best
   return HAPT_OK;
 }
 
+namespace {
+struct OneLayout {
+  size_t tmax, ftop, states, ws, total;
+};
+OneLayout one_layout(const hapt_tables *t) {
+  OneLayout y{};
+  size_t cur = 0;
+  y.tmax = cur; cur += align_up(8);
+  y.ftop = cur; cur += align_up((size_t)(t->s_max + 1) * 8);
+  y.states = cur; cur += align_up(8);
+  y.ws = cur; cur += align_up(ws_layout(t, 1).total);
+  y.total = cur;
+  return y;
+}
+}  // namespace
+
+extern "C" size_t hapt_dp_sweep_workspace_bytes(const hapt_tables *t) {
+  return t ? one_layout(t).total : 0;
+}
+
+extern "C" int hapt_dp_sweep(const hapt_tables *t, double tmax, double *F, double *N,
+                             int32_t *bp_i, int32_t *bp_o, void *work, size_t work_bytes,
+                             void *stream) {
+  if (!t || !F || !N || !bp_i || !bp_o || !work || !(tmax > 0.0)) {
+    set_error("hapt_dp_sweep: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  const OneLayout y = one_layout(t);
+  if (work_bytes < y.total) {
+    set_error("hapt_dp_sweep: workspace %zu < %zu", work_bytes, y.total);
+    return HAPT_ENOSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char *w = (char *)work;
+  double *d_tmax = (double *)(w + y.tmax);
+  HAPT_CUDA(cudaMemcpyAsync(d_tmax, &tmax, 8, cudaMemcpyHostToDevice, st));
+  // the reference's fresh output arrays: F = +inf but F[0, L+1, 0] = 0,
+  // N = 0, bp = -1 (_dp.pyx:33-41); the sweep writes every finite cell
+  hapt_dp_full full{};
+  full.F = F, full.N = N, full.bp_i = bp_i, full.bp_o = bp_o;
+  const size_t cells = (size_t)(t->s_max + 1) * (t->L + 2) * (t->G + 1);
+  fill_full<<<grid_for(cells, 256), 256, 0, st>>>(full, cells, t->L, t->G);
+  ::hapt::note_launch();
+  HAPT_LAUNCHED("fill_full");
+  Batch b = make_batch(t, d_tmax, 1, (double *)(w + y.ftop), (int64_t *)(w + y.states), &full,
+                       w + y.ws);
+  return run_sweep(b, st);
+}
+
 extern "C" int hapt_dp_walk(const hapt_tables *t, const int32_t *bp_cand, int32_t best_s,
                             int32_t *stages, int32_t *n_stages, void *stream) {
   if (!t || !bp_cand || !stages || !n_stages || best_s < 1 || best_s > t->s_max) {

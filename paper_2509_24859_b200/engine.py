@@ -365,14 +365,20 @@ class Sweeper:
         dp_sweep); returns device tensors."""
         t = self.tables
         shape = (t.s_max + 1, t.L + 2, t.G + 1)
-        F = torch.full(shape, math.inf, dtype=_F64, device=self.device)
-        F[0, t.L + 1, 0] = 0.0
-        N = torch.zeros(shape, dtype=_F64, device=self.device)
-        bpi = torch.full(shape, -1, dtype=_I32, device=self.device)
-        bpo = torch.full(shape, -1, dtype=_I32, device=self.device)
-        full = DpFull(F.data_ptr(), N.data_ptr(), bpi.data_ptr(), bpo.data_ptr(), None, None)
-        tmax = torch.tensor([t_max], dtype=_F64, device=self.device)
-        self.sweep_device(tmax, full=full)
+        if not t_max > 0:  # no span fits: the reference's fresh arrays, untouched
+            F = torch.full(shape, math.inf, dtype=_F64, device=self.device)
+            F[0, t.L + 1, 0] = 0.0
+            return (F, torch.zeros(shape, dtype=_F64, device=self.device),
+                    torch.full(shape, -1, dtype=_I32, device=self.device),
+                    torch.full(shape, -1, dtype=_I32, device=self.device))
+        F = torch.empty(shape, dtype=_F64, device=self.device)
+        N = torch.empty(shape, dtype=_F64, device=self.device)
+        bpi = torch.empty(shape, dtype=_I32, device=self.device)
+        bpo = torch.empty(shape, dtype=_I32, device=self.device)
+        ws = self._workspace(self.lib.hapt_dp_sweep_workspace_bytes(ctypes.byref(t.t)))
+        check(self.lib.hapt_dp_sweep(ctypes.byref(t.t), float(t_max), F.data_ptr(), N.data_ptr(),
+                                     bpi.data_ptr(), bpo.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     stream_ptr()))
         return F, N, bpi, bpo
 
     def backtrack(self, t_max: float, best_s: int):

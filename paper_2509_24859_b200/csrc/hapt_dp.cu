@@ -33,6 +33,9 @@
 namespace hapt {
 namespace {
 
+#ifdef HAPT_COUNT_WORK
+__device__ unsigned long long g_work[4];  // executed / admissible / improving
+#endif
 constexpr int kWarps = 8;  // warps (cells) per block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
 #ifndef HAPT_RELAX_MINB
@@ -426,6 +429,14 @@ __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const double v = __dadd_rn(tt, h[q][c]);  // tt + (2c + F)  (_dp.pyx:85)
+#ifdef HAPT_COUNT_WORK  // instrumented build only (tools/work_counts.py)
+        if (u + q < n) {
+          const bool adm = (unsigned)ex[q].z < cnt2[c] && h[q][c] != kInf;
+          atomicAdd(&g_work[0], 1ull);
+          if (adm) atomicAdd(&g_work[1], 1ull);
+          if (adm && v < bv[c]) atomicAdd(&g_work[2], 1ull);
+        }
+#endif
         if ((unsigned)ex[q].z < cnt2[c] && (!WITH_KK || kk[q][c] <= km) && v < bv[c]) {
           bv[c] = v;
           bw2[c] = (unsigned)ex[q].z;
@@ -1184,3 +1195,13 @@ extern "C" int hapt_activated_pairs(const hapt_tables *t, const double *tmax, in
   HAPT_LAUNCHED("hapt_activated_pairs");
   return HAPT_OK;
 }
+
+#ifdef HAPT_COUNT_WORK
+// instrumented build only: cumulative transition counters of the DP loop
+extern "C" int hapt_debug_work(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, hapt::g_work, sizeof(unsigned long long) * 4) == cudaSuccess
+             ? HAPT_OK
+             : HAPT_ECUDA;
+}
+#endif

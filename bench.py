@@ -394,6 +394,24 @@ def main():
             }
     except (OSError, KeyError, ValueError):
         pass
+    # the transitions the kernel actually executes (instrumented build,
+    # tools/work_counts.py: a property of the algorithm, scaled to this run)
+    try:
+        with open(os.path.join(REPO, "profiles", "dp_relax_work.json")) as fh:
+            wk = json.load(fh)[args.config]
+        if measured is not None:
+            scale = n_mine / wk["pool_candidates"]
+            ex = wk["executed_lane_transitions"] * scale * args.steps / dev_s
+            measured.update({
+                "executed_transitions_per_s": ex,
+                "executed_share_of_reference_transitions":
+                    wk["executed_lane_transitions"] / wk["reference_transitions"],
+                "admissible_share_of_executed":
+                    wk["admissible_lane_transitions"] / wk["executed_lane_transitions"],
+                "executed_fp64_frac": 2 * ex / fp64,  # one DADD + one compare each
+            })
+    except (OSError, KeyError, ValueError):
+        pass
     roofline = {
         "bound": "hbm",
         "kernel": "dp_relax (hapt_dp.cu)",

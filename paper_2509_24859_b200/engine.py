@@ -32,10 +32,6 @@ def default_device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _dev_tensor(values, dtype, device):
-    return torch.as_tensor(np.asarray(values), dtype=dtype).to(device, non_blocking=False)
-
-
 class DeviceTables:
     """hapt_tables for one planning instance."""
 
@@ -81,18 +77,27 @@ class DeviceTables:
     def build(self, desc_arrays: dict, scalars: dict) -> "DeviceTables":
         """Run K1 from host description arrays (hapt_model_desc)."""
         dev = self.device
-        keep = {}
         d = ModelDesc()
         d.L, d.n_meshes, d.n_opts, d.G = self.L, self.n_meshes, self.n_opts, self.G
         f64 = ("layer_flops", "layer_params", "layer_bbytes", "mesh_peak", "mesh_mem",
                "mesh_intra_bw", "mesh_inter_bw", "cross_bw_next", "ovr_vals")
+        # every description array in one host buffer and one H2D copy
+        parts, offs, cur = [], {}, 0
         for name, arr in desc_arrays.items():
             if arr is None:
-                setattr(d, name, None)
                 continue
-            t = _dev_tensor(arr, _F64 if name in f64 else _I32, dev)
-            keep[name] = t
-            setattr(d, name, t.data_ptr())
+            a = np.ascontiguousarray(arr, dtype=np.float64 if name in f64 else np.int32)
+            offs[name] = cur
+            parts.append((cur, a.view(np.uint8).reshape(-1)))
+            cur += (a.nbytes + 15) // 16 * 16
+        host = np.zeros(max(cur, 16), dtype=np.uint8)
+        for off, raw in parts:
+            host[off : off + raw.size] = raw
+        blob = torch.from_numpy(host).to(dev)
+        base = blob.data_ptr()
+        for name in desc_arrays:
+            setattr(d, name, base + offs[name] if name in offs else None)
+        keep = {"blob": blob}
         for name, val in scalars.items():
             setattr(d, name, val)
         check(self.lib.hapt_tables_build(ctypes.byref(self.t), ctypes.byref(d), stream_ptr()))

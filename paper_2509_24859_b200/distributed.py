@@ -53,28 +53,41 @@ class PoolSharding:
         self.collective_calls += 1
         return torch.stack(out).cpu()
 
-    def evaluate_sharded(self, sweeper, pool: np.ndarray, todo, num_microbatches: int):
+    def evaluate_sharded(self, sweeper, pool: np.ndarray, todo, num_microbatches: int,
+                         want_ftop: bool = False):
         """Evaluate pool[todo] with each rank taking todo[rank::world]; every
-        rank returns the full (tstar, best_s, states) in `todo` order."""
+        rank returns the full (tstar, best_s, states) in `todo` order, plus
+        F[s,1,G] per candidate when want_ftop (search_batches)."""
         todo = list(todo)
         mine = self.shard(todo)
         width = (len(todo) + self.world - 1) // self.world
+        s1 = sweeper.tables.s_max + 1 if want_ftop else 0
+        cols = 3 + s1
         if mine:
-            res = sweeper.evaluate(pool[mine], num_microbatches)
-            loc = np.stack([res.tstar.view(np.int64), res.best_s.astype(np.int64),
-                            res.states.astype(np.int64)], axis=1)
+            res = (sweeper.evaluate(pool[mine], num_microbatches, keep_ftop=True) if want_ftop
+                   else sweeper.evaluate(pool[mine], num_microbatches))
+            parts = [res.tstar.view(np.int64)[:, None], res.best_s.astype(np.int64)[:, None],
+                     res.states.astype(np.int64)[:, None]]
+            if want_ftop:
+                parts.append(np.ascontiguousarray(res.ftop).view(np.int64))
+            loc = np.concatenate(parts, axis=1)
         else:
-            loc = np.zeros((0, 3), dtype=np.int64)
+            loc = np.zeros((0, cols), dtype=np.int64)
         allv = self._all_gather(torch.from_numpy(np.ascontiguousarray(loc)), max(width, 1)).numpy()
         tstar = np.empty(len(todo))
         best_s = np.empty(len(todo), dtype=np.int64)
         states = np.empty(len(todo), dtype=np.int64)
+        ftop = np.empty((len(todo), s1)) if want_ftop else None
         for r in range(self.world):
             pos = np.arange(r, len(todo), self.world)
             blk = allv[r, : len(pos)]
             tstar[pos] = blk[:, 0].view(np.float64)
             best_s[pos] = blk[:, 1]
             states[pos] = blk[:, 2]
+            if want_ftop:
+                ftop[pos] = np.ascontiguousarray(blk[:, 3:]).view(np.float64)
+        if want_ftop:
+            return tstar, best_s, states, ftop
         return tstar, best_s, states
 
     def allreduce_argmin(self, tstar: float, index: int):

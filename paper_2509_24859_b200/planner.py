@@ -283,6 +283,13 @@ class CandidateEvaluator:
                 self._bp_bytes += need
                 for pos, i in enumerate(todo):
                     self._bp_of[i] = (res, pos)
+        elif self.ftop is not None:
+            ts, bs, st, ft = self.dist.evaluate_sharded(self.tables.sweeper, self.pool, todo,
+                                                        self.B, want_ftop=True)
+            self.ftop[todo] = ft
+            self.tstar[todo] = ts
+            self.best_s[todo] = bs
+            self.states[todo] = st
         else:
             ts, bs, st = self.dist.evaluate_sharded(self.tables.sweeper, self.pool, todo, self.B)
             self.tstar[todo] = ts
@@ -623,7 +630,7 @@ def _score(ftop: np.ndarray, tmax: np.ndarray, B: int):
 
 def search_batches(store: ProfileStore, costs: BoundaryCost, batch_sizes: Sequence[int],
                    epsilon: float = 0.05, batch_size: Optional[int] = None,
-                   optimized: bool = True) -> dict:
+                   optimized: bool = True, dist=None) -> dict:
     """search() for several microbatch counts from one set of DP sweeps
     (SURVEY.md §8(f)3).  The DP tables F, N (_dp.pyx:48-95) depend on t_max
     only, so every candidate is swept once and scored for each B afterwards
@@ -631,7 +638,8 @@ def search_batches(store: ProfileStore, costs: BoundaryCost, batch_sizes: Sequen
     the reference's binary search (planner.py:456-474) is replayed once; each
     B then keeps its own t_e cut and merge.  Returns {B: plan}; every plan and
     its search_stats (but wall_time_s, which is the shared total) equal
-    search(store, costs, B, epsilon, batch_size=batch_size, optimized=...)."""
+    search(store, costs, B, epsilon, batch_size=batch_size, optimized=...).
+    `dist` (PoolSharding) shards every batch across ranks as in search()."""
     began = time.perf_counter()
     Bs = [int(b) for b in batch_sizes]
     if not Bs or min(Bs) < 1:
@@ -639,7 +647,7 @@ def search_batches(store: ProfileStore, costs: BoundaryCost, batch_sizes: Sequen
     tables = DpTables(store, costs)
     pool = candidate_tmax(store)
     n = len(pool)
-    ev = CandidateEvaluator(tables, pool, Bs[0], keep_ftop=True)
+    ev = CandidateEvaluator(tables, pool, Bs[0], dist=dist, keep_ftop=True)
     if optimized:
         lo, _, _, probed = bidirectional_prune_replay(ev, Bs[0])
         t_lo = np.array([pool[lo]])

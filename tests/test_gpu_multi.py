@@ -30,7 +30,7 @@ def _worker(rank, world, port, names, out_q):
 
     from helpers import assert_plan_equal, build, expected, expected_arrays, load_json, plan_dict
     from paper_2509_24859_b200.distributed import PoolSharding
-    from paper_2509_24859_b200.planner import search, sweep_pool
+    from paper_2509_24859_b200.planner import search, search_batches, sweep_pool
 
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world)
@@ -48,6 +48,12 @@ def _worker(rank, world, port, names, out_q):
                 feas = np.where(arr["best_s"] >= 0)[0]
                 want = int(feas[np.lexsort((arr["pool"][feas], arr["tstar"][feas]))[0]])
                 assert winner == want, (winner, want)
+                # sharded microbatch-count sweep == per-B sharded search
+                many = search_batches(store, costs, [B, 2 * B], epsilon=eps, batch_size=4,
+                                      dist=sh)
+                assert_plan_equal(plan_dict(many[B]), expected(name)["plan"])
+                one = search(store, costs, 2 * B, epsilon=eps, batch_size=4, dist=sh)
+                assert_plan_equal(plan_dict(many[2 * B]), plan_dict(one))
             except AssertionError as exc:
                 errors.append(f"{name}: {exc}")
     finally:

@@ -48,11 +48,12 @@ class SweepPoint:
 def microbatch_sweep(build_ops: Callable[[int], list], cluster,
                      points: Sequence[tuple] = DEFAULT_POINTS, model: CostModel | None = None,
                      layers_per_module_unit: int = 1, imbalance_ratio: float = 3.0,
-                     epsilon: float = 0.05, z: int = 1, batch_size=None) -> list:
+                     epsilon: float = 0.05, z: int = 1, batch_size=None, dist=None) -> list:
     """Plan every (mb_size, B) point.  `build_ops(mb_size)` returns the
     operator sequence of one microbatch of that size (e.g.
     workloads.llama_like_ops(b=mb_size) or generate_gpt_sequence(GptConfig(...,
-    mb_size=...))).  Returns SweepPoints in the order of `points`."""
+    mb_size=...))).  Returns SweepPoints in the order of `points`.  `dist`
+    (PoolSharding) shards every candidate batch across ranks."""
     by_mb: dict = {}
     for mb, B in points:
         by_mb.setdefault(int(mb), []).append(int(B))
@@ -68,9 +69,10 @@ def microbatch_sweep(build_ops: Callable[[int], list], cluster,
         costs = boundary_costs(layers, cluster)
         if len(set(Bs)) > 1:
             plans = search_batches(store, costs, sorted(set(Bs)), epsilon=epsilon,
-                                   batch_size=batch_size)
+                                   batch_size=batch_size, dist=dist)
         else:
-            plans = {Bs[0]: search(store, costs, Bs[0], epsilon=epsilon, batch_size=batch_size)}
+            plans = {Bs[0]: search(store, costs, Bs[0], epsilon=epsilon, batch_size=batch_size,
+                                   dist=dist)}
         for B in Bs:
             done[(mb, B)] = SweepPoint(mb, B, layers, plans[B])
     return [done[(int(mb), int(B))] for mb, B in points]

@@ -62,7 +62,7 @@ int cpl_for(const hapt_tables *t, int n_cand) {
 #define HAPT_U4 2
 #endif
 #ifndef HAPT_U2
-#define HAPT_U2 4  // 4 or 8 (a 32-entry stage must be a multiple)
+#define HAPT_U2 4  // 2, 4 or 8 (a 32-entry stage must be a multiple)
 #endif
 template <int CPL>
 struct Unroll {

@@ -18,6 +18,7 @@ bit for bit (tests/test_search_parity.py).
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
@@ -332,6 +333,9 @@ def _batch_depth(tables: DpTables, pool_len: int) -> int:
     """Speculation depth: enough probes per batch to fill the GPU.  A batch of
     32 candidates needs one warp per DP cell per layer; ~40k resident-warp
     slots on 148 SMs are the target."""
+    env = os.environ.get("HAPT_SEARCH_DEPTH")  # experiments
+    if env:
+        return max(1, int(env))
     cells = max(1, tables.L * tables.G)
     groups = max(1, math.ceil(40_000 / cells))
     want = groups * 32

@@ -535,116 +535,65 @@ struct PySum {
   }
 };
 
-// One stage's op intervals in program order.  Starts are non-decreasing
-// (start = max(previous end, dependency)), and equal starts only follow a
-// zero-length op, so this is the order sorted() gives _interval_union.
-struct StageSrc {
+// Sweep-line cursor over one serial interval list: a stage's ops in program
+// order (start = max(previous end, dependency) >= previous end) or one link
+// direction's transfers in microbatch order (endCF[i] = max(endF[i],
+// endCF[i-1]) + c, so each starts after the previous one ends).  The list's
+// boundaries lo0 <= hi0 <= lo1 <= hi1 <= ... are visited in order; empty
+// intervals (hi <= lo) are skipped, as _interval_union drops them.
+template <class Ids>
+struct Serial {
   const double *st, *en;
-  int64_t base;  // node id of (F, mb 1) on this stage
-  int N, B, pos;
-  __device__ bool next(double &lo, double &hi) {
-    if (pos >= 2 * B) return false;
+  Ids ids;
+  int n, k;            // intervals, next interval to open
+  bool open;           // inside interval k-1
+  double x, hi;        // next boundary; end of the open interval
+  __device__ void load() {  // x = start of the next non-empty interval
+    for (; k < n; ++k) {
+      const int64_t id = ids(k);
+      const double lo = st[id];
+      hi = en[id];
+      if (hi > lo) {
+        x = lo;
+        ++k;
+        return;
+      }
+    }
+    x = kInf;
+  }
+  __device__ void init() {
+    k = 0;
+    open = false;
+    load();
+  }
+  __device__ void step(double at) {  // apply every boundary at coordinate `at`
+    while (x == at) {
+      if (open) {
+        open = false;
+        load();
+      } else {
+        open = true;
+        x = hi;
+      }
+    }
+  }
+};
+
+struct StageIds {  // op q of a stage in program order -> node id
+  int64_t base;    // node id of (F, mb 1) on this stage
+  int N, B;
+  __device__ int64_t operator()(int q) const {
     bool isF;
-    const int mb = decode_op(pos++, N, B, isF);
-    const int64_t id = base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
-    lo = st[id];
-    hi = en[id];
-    return true;
+    const int mb = decode_op(q, N, B, isF);
+    return base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
   }
 };
 
-// One link's transfers: forward (mb order) and backward (mb order) lists are
-// each sorted; merged by (lo, hi) as sorted() orders the concatenation.
-struct LinkSrc {
-  const double *st, *en;
-  int64_t base;  // node id of (CF, mb 1) on this link
-  int B, i, j;   // next forward / backward microbatch (1-based)
-  __device__ bool next(double &lo, double &hi) {
-    const bool hf = i <= B, hb = j <= B;
-    if (!hf && !hb) return false;
-    double flo = 0, fhi = 0, blo = 0, bhi = 0;
-    if (hf) {
-      flo = st[base + 2 * (int64_t)(i - 1)];
-      fhi = en[base + 2 * (int64_t)(i - 1)];
-    }
-    if (hb) {
-      blo = st[base + 2 * (int64_t)(j - 1) + 1];
-      bhi = en[base + 2 * (int64_t)(j - 1) + 1];
-    }
-    if (hf && (!hb || flo < blo || (flo == blo && fhi <= bhi))) {
-      lo = flo, hi = fhi, ++i;
-    } else {
-      lo = blo, hi = bhi, ++j;
-    }
-    return true;
-  }
+struct LinkIds {  // transfer of microbatch i+1 in one direction -> node id
+  int64_t base;   // node id of (CF, mb 1) on this link
+  int dir;        // 0 forward, 1 backward
+  __device__ int64_t operator()(int i) const { return base + 2 * (int64_t)i + dir; }
 };
-
-// _interval_union over a sorted source (empty intervals dropped, touching
-// ones merged)
-template <class Src>
-struct Union {
-  Src src;
-  double clo = 0, chi = 0;
-  bool has = false;
-  __device__ bool next(double &lo, double &hi) {
-    double a, b;
-    while (src.next(a, b)) {
-      if (b <= a) continue;
-      if (!has) {
-        clo = a, chi = b, has = true;
-        continue;
-      }
-      if (a <= chi) {
-        chi = b > chi ? b : chi;
-        continue;
-      }
-      lo = clo, hi = chi;
-      clo = a, chi = b;
-      return true;
-    }
-    if (!has) return false;
-    lo = clo, hi = chi, has = false;
-    return true;
-  }
-};
-
-// _intersect of two sorted disjoint interval streams
-template <class A, class B>
-struct Inter {
-  A a;
-  B b;
-  double alo = 0, ahi = 0, blo = 0, bhi = 0;
-  bool ha = false, hb = false, primed = false;
-  __device__ bool next(double &lo, double &hi) {
-    if (!primed) {
-      ha = a.next(alo, ahi);
-      hb = b.next(blo, bhi);
-      primed = true;
-    }
-    while (ha && hb) {
-      const double l = blo > alo ? blo : alo, h = bhi < ahi ? bhi : ahi;
-      const bool emit = h > l;
-      if (ahi <= bhi)
-        ha = a.next(alo, ahi);
-      else
-        hb = b.next(blo, bhi);
-      if (emit) {
-        lo = l, hi = h;
-        return true;
-      }
-    }
-    return false;
-  }
-};
-
-template <class G>
-__device__ double total_of(G gen) {  // _total: sum(hi - lo)
-  PySum sum;
-  double lo, hi;
-  while (gen.next(lo, hi)) sum.add(__dadd_rn(hi, -lo));
-  return sum.any ? sum.value() : 0.0;
-}
 
 // Three thread ranges, so that a warp's threads run the same kind of row
 // (a mixed warp serialises a long link walk behind short stage rows):
@@ -734,19 +683,45 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     PySum f;
     for (int q = 0; q < B; ++q) f.add(c);
     const double ft = f.value();
+    // One sweep over the four serial lists.  busy = _interval_union(forward
+    // + backward transfers) is where either direction is open; its pieces are
+    // the maximal runs of that (touching transfers merge: all boundaries at a
+    // coordinate apply before the state is read).  _intersect(_intersect(busy,
+    // stage s), stage s+1) yields exactly the maximal runs where busy and both
+    // stages are open, each as [max of starts, min of ends] — the boundary
+    // coordinates here — in increasing order, so both sums see the
+    // reference's terms in the reference's order.
     const int64_t lbase = nb + 2 * (int64_t)S * B + 2 * (int64_t)s * B;
-    Union<LinkSrc> link{LinkSrc{st, en, lbase, B, 1, 1}};
-    const double tot = total_of(link);
-    double ratio = 1.0;
-    if (tot > 0.0) {
-      Union<StageSrc> u0{StageSrc{st, en, nb + 2 * (int64_t)s * B, counts[x], B, 0}};
-      Union<StageSrc> u1{StageSrc{st, en, nb + 2 * (int64_t)(s + 1) * B, counts[x + 1], B, 0}};
-      Inter<Inter<Union<LinkSrc>, Union<StageSrc>>, Union<StageSrc>> both{
-          Inter<Union<LinkSrc>, Union<StageSrc>>{Union<LinkSrc>{LinkSrc{st, en, lbase, B, 1, 1}},
-                                                 u0},
-          u1};
-      ratio = __ddiv_rn(total_of(both), tot);
+    Serial<LinkIds> cf{st, en, LinkIds{lbase, 0}, B}, cb{st, en, LinkIds{lbase, 1}, B};
+    Serial<StageIds> u0{st, en, StageIds{nb + 2 * (int64_t)s * B, counts[x], B}, 2 * B};
+    Serial<StageIds> u1{st, en, StageIds{nb + 2 * (int64_t)(s + 1) * B, counts[x + 1], B}, 2 * B};
+    cf.init();
+    cb.init();
+    u0.init();
+    u1.init();
+    PySum tot, both;
+    bool in_busy = false, in_all = false;
+    double busy0 = 0, all0 = 0;
+    while (cf.x < kInf || cb.x < kInf) {  // no pieces outside busy
+      const double at = fmin(fmin(cf.x, cb.x), fmin(u0.x, u1.x));
+      cf.step(at);
+      cb.step(at);
+      u0.step(at);
+      u1.step(at);
+      const bool b = cf.open || cb.open;
+      const bool a = b && u0.open && u1.open;
+      if (a != in_all) {
+        if (a) all0 = at; else both.add(__dadd_rn(at, -all0));
+        in_all = a;
+      }
+      if (b != in_busy) {
+        if (b) busy0 = at; else tot.add(__dadd_rn(at, -busy0));
+        in_busy = b;
+      }
     }
+    const double total = tot.any ? tot.value() : 0.0;
+    const double ratio =
+        total > 0.0 ? __ddiv_rn(both.any ? both.value() : 0.0, total) : 1.0;
     lr[0] = ft;
     lr[1] = ft;  // backward transfers carry the same boundary time
     lr[2] = ratio;

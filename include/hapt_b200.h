@@ -287,6 +287,28 @@ int hapt_analyze_1f1b(int32_t n_plans, int32_t total_stages, const int32_t *stag
                       int32_t *peak_inflight, double *link_rep, double *steady_rate,
                       void *stream);
 
+/* The same two calls over a "trace" layout that a batched simulation writes
+ * with whole-sector stores (the analysis path of PlanBatch.analyze): pairs
+ * {start, end} of doubles, trace 16-byte aligned, plan p's pairs from pair
+ * index trace_off[p] on (double index 2*trace_off[p]):
+ *   stage s, op q of its 1F1B program (q in [0, 2B)):  pair 2sB + q
+ *   link l, forward transfer of microbatch i:          pair 2SB + 2lB + i - 1
+ *   link l, backward transfer of microbatch i:         pair 2SB + (2l+1)B + i - 1
+ * B(4S - 2) pairs per plan (the reference's sink node is the makespan).
+ * Figures equal hapt_sim_1f1b / hapt_analyze_1f1b's bit for bit. */
+int hapt_sim_1f1b_trace(int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
+                        const double *t_bwd, const double *comm, const int32_t *counts,
+                        const int32_t *num_mb, double *makespan, double *trace,
+                        const int64_t *trace_off, int32_t ring_depth, int32_t *status,
+                        void *work, size_t work_bytes, void *stream);
+int hapt_analyze_1f1b_trace(int32_t n_plans, int32_t total_stages, const int32_t *stage_off,
+                            const double *t_fwd, const double *t_bwd, const double *comm,
+                            const int32_t *counts, const int32_t *num_mb,
+                            const double *mem_act, const double *trace,
+                            const int64_t *trace_off, const int32_t *status,
+                            double *stage_rep, int32_t *peak_inflight, double *link_rep,
+                            double *steady_rate, void *stream);
+
 /* Longest-path start times of an arbitrary DAG given as successor CSR:
  * start[v] = max_u (start[u] + duration[u]). processed [1] = number of nodes
  * reached (< n_nodes <=> cycle). */

@@ -154,6 +154,16 @@ _SIGNATURES = {
         [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
          c_vp, c_vp, c_vp, c_vp],
     ),
+    "hapt_sim_1f1b_trace": (
+        c_i32,
+        [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_sz,
+         c_vp],
+    ),
+    "hapt_analyze_1f1b_trace": (
+        c_i32,
+        [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+         c_vp, c_vp, c_vp],
+    ),
     "hapt_dag_workspace_bytes": (c_sz, [c_i32]),
     "hapt_dag_longest_path": (
         c_i32,

@@ -106,12 +106,63 @@ __device__ __forceinline__ int decode_op(int pos, int N, int B, bool &isF) {
   return steady + (q - 2 * steady) + 1;
 }
 
+// Inverse of decode_op: program position of (mb, F or B) on a stage.
+__device__ __forceinline__ int encode_op(int mb, bool isF, int N, int B) {
+  const int steady = B - N;
+  if (isF) return mb <= N ? mb - 1 : N + 2 * (mb - N) - 1;
+  return mb <= steady ? N + 2 * (mb - 1) : N + 2 * steady + (mb - steady - 1);
+}
+
+// Where a simulation puts per-node times (all pointers null: makespan only).
+//   Reference numbering (simulation.py:103-111), start / end arrays: stage s
+//     op (mb, F/B) at nb + 2(sB + mb - 1) + {0, 1}, link l transfer (mb,
+//     fwd/bwd) at nb + 2SB + 2(lB + mb - 1) + {0, 1}, the sink last.
+//   Trace layout, double2 {start, end}: stage s's ops in program order at
+//     nb + 2sB + q, link l's forward transfers at nb + 2SB + 2lB + mb - 1 and
+//     its backward ones B further on; no sink (it is the makespan).  A
+//     thread writes each of its lists front to back, so every 32-byte sector
+//     is complete after two consecutive stores instead of collecting four
+//     scattered ones (partial sectors evicted from L2 cost a DRAM read).
+// nb = off[p] in either layout.
+struct NodeOut {
+  double *start, *end;
+  double2 *trace;
+  const int64_t *off;
+  __device__ bool on() const { return start != nullptr || trace != nullptr; }
+  __device__ void op(int64_t nb, int B, int s, int mb, bool isF, int q, double a,
+                     double e) const {
+    if (trace) {
+      trace[nb + 2 * (int64_t)s * B + q] = make_double2(a, e);
+    } else {
+      const int64_t id = nb + 2 * ((int64_t)s * B + (mb - 1)) + (isF ? 0 : 1);
+      start[id] = a;
+      end[id] = e;
+    }
+  }
+  __device__ void xfer(int64_t nb, int S, int B, int l, int dir, int mb, double a,
+                       double e) const {
+    const int64_t base = nb + 2 * (int64_t)S * B + 2 * (int64_t)l * B;
+    if (trace) {
+      trace[base + (int64_t)dir * B + (mb - 1)] = make_double2(a, e);
+    } else {
+      const int64_t id = base + 2 * (int64_t)(mb - 1) + dir;
+      start[id] = a;
+      end[id] = e;
+    }
+  }
+  __device__ void sink(int64_t nb, int S, int B, double mk) const {
+    if (trace) return;
+    const int64_t id = nb + 2 * (int64_t)S * B + 2 * (int64_t)(S - 1) * B;
+    start[id] = mk;
+    end[id] = mk;
+  }
+};
+
 __global__ void k_sim(int n_plans, const int32_t *perm, const int32_t *n_perm,
                       const int32_t *stage_off, const double *t_fwd,
                       const double *t_bwd, const double *comm, const int32_t *counts,
-                      const int32_t *num_mb, double *makespan, double *node_start,
-                      double *node_end, const int64_t *node_off, int R, double *ring,
-                      int32_t *status) {
+                      const int32_t *num_mb, double *makespan, NodeOut out, int R,
+                      double *ring, int32_t *status) {
   // all plans (perm == NULL) or the n_perm[0] plans listed in perm
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (perm ? *n_perm : n_plans)) return;
@@ -139,8 +190,8 @@ __global__ void k_sim(int n_plans, const int32_t *perm, const int32_t *n_perm,
   }
   // FIFOs: link s forward at ring[(b0+s)*2R + slot], backward at +R
   double *rf = ring + (size_t)b0 * 2 * R;
-  const int64_t nb = node_off ? node_off[p] : 0;
-  const bool want_nodes = node_start != nullptr;
+  const bool want_nodes = out.on();
+  const int64_t nb = want_nodes ? out.off[p] : 0;
   double mk = 0.0;
   int remaining = S;
   for (int s = 0; s < S; ++s) remaining -= (2 * B == 0);
@@ -168,11 +219,7 @@ __global__ void k_sim(int n_plans, const int32_t *perm, const int32_t *n_perm,
         const double en = __dadd_rn(st, d);
         prev[s] = en;
         mk = fmax(mk, en);
-        if (want_nodes) {
-          const int64_t id = nb + 2 * ((int64_t)s * B + (mb - 1)) + (isF ? 0 : 1);
-          node_start[id] = st;
-          node_end[id] = en;
-        }
+        if (want_nodes) out.op(nb, B, s, mb, isF, pos[s], st, en);
         if (isF) {
           fdone[s] = mb;
           if (s < S - 1) {  // forward transfer on link s
@@ -181,11 +228,7 @@ __global__ void k_sim(int n_plans, const int32_t *perm, const int32_t *n_perm,
             lcf[s] = ce;
             mk = fmax(mk, ce);
             rf[(size_t)s * 2 * R + (mb % R)] = ce;
-            if (want_nodes) {
-              const int64_t id = nb + 2 * (int64_t)S * B + 2 * ((int64_t)s * B + (mb - 1));
-              node_start[id] = cs;
-              node_end[id] = ce;
-            }
+            if (want_nodes) out.xfer(nb, S, B, s, 0, mb, cs, ce);
           }
         } else {
           bdone[s] = mb;
@@ -195,12 +238,7 @@ __global__ void k_sim(int n_plans, const int32_t *perm, const int32_t *n_perm,
             lcb[s - 1] = ce;
             mk = fmax(mk, ce);
             rf[(size_t)(s - 1) * 2 * R + R + (mb % R)] = ce;
-            if (want_nodes) {
-              const int64_t id =
-                  nb + 2 * (int64_t)S * B + 2 * ((int64_t)(s - 1) * B + (mb - 1)) + 1;
-              node_start[id] = cs;
-              node_end[id] = ce;
-            }
+            if (want_nodes) out.xfer(nb, S, B, s - 1, 1, mb, cs, ce);
           }
         }
         ++pos[s];
@@ -214,11 +252,7 @@ __global__ void k_sim(int n_plans, const int32_t *perm, const int32_t *n_perm,
       return;
     }
   }
-  if (want_nodes) {
-    const int64_t sink = nb + 2 * (int64_t)S * B + 2 * (int64_t)(S - 1) * B;
-    node_start[sink] = mk;
-    node_end[sink] = mk;
-  }
+  if (want_nodes) out.sink(nb, S, B, mk);
   makespan[p] = mk;
   status[p] = HAPT_OK;
 }
@@ -317,8 +351,7 @@ template <int S>
 __global__ void __launch_bounds__(SimCfg<S>::threads)
     k_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
             const double *t_bwd, const double *comm, const int32_t *counts,
-            const int32_t *num_mb, double *makespan, int32_t *status, double *node_start,
-            double *node_end, const int64_t *node_off) {
+            const int32_t *num_mb, double *makespan, int32_t *status, NodeOut out) {
   extern __shared__ double ring[];  // [(S-1) links][2 dirs][kRing][threads]
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -353,8 +386,8 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
   }
   double mk = 0.0;
   // optional per-node times in the reference numbering (simulation.py:103-111)
-  const bool nodes = node_start != nullptr;
-  const int64_t nb = nodes ? node_off[p] : 0, cf0 = nb + 2 * (int64_t)S * B;
+  const bool nodes = out.on();
+  const int64_t nb = nodes ? out.off[p] : 0;
   int remaining = S;
   while (remaining > 0) {
     bool progress = false;
@@ -376,11 +409,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
           const double en = __dadd_rn(st, isF ? tf[s] : tb[s]);
           prev[s] = en;
           mk = fmax(mk, en);
-          if (nodes) {
-            const int64_t id = nb + 2 * ((int64_t)s * B + (mb - 1)) + (isF ? 0 : 1);
-            node_start[id] = st;
-            node_end[id] = en;
-          }
+          if (nodes) out.op(nb, B, s, mb, isF, pos[s], st, en);
           if (isF) {
             fd[s] = mb;
             if (s < S - 1) {  // forward transfer on link s (simulation.py:130-140)
@@ -389,11 +418,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
               lcf[s] = ce;
               mk = fmax(mk, ce);
               slot(s, 0, mb) = ce;
-              if (nodes) {
-                const int64_t id = cf0 + 2 * ((int64_t)s * B + (mb - 1));
-                node_start[id] = cs;
-                node_end[id] = ce;
-              }
+              if (nodes) out.xfer(nb, S, B, s, 0, mb, cs, ce);
             }
           } else {
             bd[s] = mb;
@@ -403,11 +428,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
               lcb[s - 1] = ce;
               mk = fmax(mk, ce);
               slot(s - 1, 1, mb) = ce;
-              if (nodes) {
-                const int64_t id = cf0 + 2 * ((int64_t)(s - 1) * B + (mb - 1)) + 1;
-                node_start[id] = cs;
-                node_end[id] = ce;
-              }
+              if (nodes) out.xfer(nb, S, B, s - 1, 1, mb, cs, ce);
             }
           }
           if (++pos[s] == 2 * B) --remaining;
@@ -420,11 +441,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
       return;
     }
   }
-  if (nodes) {  // the sink
-    const int64_t sink = cf0 + 2 * (int64_t)(S - 1) * B;
-    node_start[sink] = mk;
-    node_end[sink] = mk;
-  }
+  if (nodes) out.sink(nb, S, B, mk);
   makespan[p] = mk;
   status[p] = HAPT_OK;
 }
@@ -491,8 +508,8 @@ __global__ void k_sim_retry(int n_plans, const int32_t *status, int32_t *perm, i
 template <int S>
 void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
                   const double *t_bwd, const double *comm, const int32_t *counts,
-                  const int32_t *num_mb, double *makespan, int32_t *status, double *node_start,
-                  double *node_end, const int64_t *node_off, cudaStream_t st) {
+                  const int32_t *num_mb, double *makespan, int32_t *status, NodeOut out,
+                  cudaStream_t st) {
   if (n <= 0) return;
   using C = SimCfg<S>;
   static bool attr = false;
@@ -501,8 +518,8 @@ void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const do
     attr = true;
   }
   k_sim_s<S><<<grid_for(n, C::threads), C::threads, C::smem, st>>>(
-      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, node_start,
-      node_end, node_off); ::hapt::note_launch();
+      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, out);
+  ::hapt::note_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -541,20 +558,18 @@ struct PySum {
 // endCF[i-1]) + c, so each starts after the previous one ends).  The list's
 // boundaries lo0 <= hi0 <= lo1 <= hi1 <= ... are visited in order; empty
 // intervals (hi <= lo) are skipped, as _interval_union drops them.
-template <class Ids>
+template <class At>
 struct Serial {
-  const double *st, *en;
-  Ids ids;
+  At at;               // interval k -> {lo, hi}
   int n, k;            // intervals, next interval to open
   bool open;           // inside interval k-1
   double x, hi;        // next boundary; end of the open interval
   __device__ void load() {  // x = start of the next non-empty interval
     for (; k < n; ++k) {
-      const int64_t id = ids(k);
-      const double lo = st[id];
-      hi = en[id];
-      if (hi > lo) {
-        x = lo;
+      const double2 v = at(k);
+      hi = v.y;
+      if (v.y > v.x) {
+        x = v.x;
         ++k;
         return;
       }
@@ -566,8 +581,8 @@ struct Serial {
     open = false;
     load();
   }
-  __device__ void step(double at) {  // apply every boundary at coordinate `at`
-    while (x == at) {
+  __device__ void step(double c) {  // apply every boundary at coordinate c
+    while (x == c) {
       if (open) {
         open = false;
         load();
@@ -579,20 +594,43 @@ struct Serial {
   }
 };
 
-struct StageIds {  // op q of a stage in program order -> node id
-  int64_t base;    // node id of (F, mb 1) on this stage
+// Node times as a simulation wrote them (NodeOut's two layouts).
+struct NodeIn {
+  const double *start, *end;
+  const double2 *trace;
+  const int64_t *off;
+};
+
+template <bool TRACE>
+struct StageAt {  // op q of a stage in program order -> {start, end}
+  NodeIn in;
+  int64_t base;   // nb + 2sB
   int N, B;
-  __device__ int64_t operator()(int q) const {
-    bool isF;
-    const int mb = decode_op(q, N, B, isF);
-    return base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
+  __device__ double2 operator()(int q) const {
+    if constexpr (TRACE) {
+      return __ldg(in.trace + base + q);
+    } else {
+      bool isF;
+      const int mb = decode_op(q, N, B, isF);
+      const int64_t id = base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
+      return make_double2(in.start[id], in.end[id]);
+    }
   }
 };
 
-struct LinkIds {  // transfer of microbatch i+1 in one direction -> node id
-  int64_t base;   // node id of (CF, mb 1) on this link
-  int dir;        // 0 forward, 1 backward
-  __device__ int64_t operator()(int i) const { return base + 2 * (int64_t)i + dir; }
+template <bool TRACE>
+struct LinkAt {  // transfer of microbatch i+1 in one direction -> {start, end}
+  NodeIn in;
+  int64_t base;   // nb + 2SB + 2lB
+  int dir, B;     // 0 forward, 1 backward
+  __device__ double2 operator()(int i) const {
+    if constexpr (TRACE) {
+      return __ldg(in.trace + base + (int64_t)dir * B + i);
+    } else {
+      const int64_t id = base + 2 * (int64_t)i + dir;
+      return make_double2(in.start[id], in.end[id]);
+    }
+  }
 };
 
 // Three thread ranges, so that a warp's threads run the same kind of row
@@ -601,11 +639,11 @@ struct LinkIds {  // transfer of microbatch i+1 in one direction -> node id
 //   [T, 2T)       the link row behind packed stage x (NaN on a plan's last stage)
 //   [2T, 2T + P)  steady_state_rate of plan p
 // (T = total stages, P = plans; plan p owns stages [stage_off[p], stage_off[p+1])).
+template <bool TRACE>
 __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t_fwd,
                           const double *t_bwd, const double *comm, const int32_t *counts,
-                          const int32_t *num_mb, const double *mem_act,
-                          const double *node_start, const double *node_end,
-                          const int64_t *node_off, const int32_t *status, double *stage_rep,
+                          const int32_t *num_mb, const double *mem_act, NodeIn in,
+                          const int32_t *status, double *stage_rep,
                           int32_t *peak_inflight, double *link_rep, double *steady_rate) {
   const long T = stage_off[n_plans];
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -628,8 +666,7 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
   const double nan = __longlong_as_double(0x7ff8000000000000ll);
   const bool failed = status && status[p] != HAPT_OK;
   const int B = num_mb[p];
-  const int64_t nb = node_off[p];
-  const double *st = node_start, *en = node_end;
+  const int64_t nb = in.off[p];
   if (role == 0) {  // -- stage row (simulation.py:331-358) --
     if (failed) {
       for (int q = 0; q < 6; ++q) stage_rep[(size_t)x * 6 + q] = nan;
@@ -640,24 +677,20 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     const int64_t base = nb + 2 * (int64_t)s * B;
     PySum busy, steady;
     int inflight = 0, peak = 0;
-    double first_start = 0, last_end = 0, steady_start = 0, steady_end = 0;
     const int w0 = N, w1 = N + 2 * (B - N);  // steady ops [w0, w1)
     for (int q = 0; q < 2 * B; ++q) {
       bool isF;
-      const int mb = decode_op(q, N, B, isF);
-      const int64_t id = base + 2 * (int64_t)(mb - 1) + (isF ? 0 : 1);
+      decode_op(q, N, B, isF);
       const double d = isF ? t_fwd[x] : t_bwd[x];
       busy.add(d);
-      if (q == 0) first_start = st[id];
-      if (q == 2 * B - 1) last_end = en[id];
-      if (q >= w0 && q < w1) {
-        steady.add(d);
-        if (q == w0) steady_start = st[id];
-        if (q == w1 - 1) steady_end = en[id];
-      }
+      if (q >= w0 && q < w1) steady.add(d);
       inflight += isF ? 1 : -1;
       peak = inflight > peak ? inflight : peak;
     }
+    const StageAt<TRACE> at{in, base, N, B};
+    const double first_start = at(0).x, last_end = at(2 * B - 1).y;
+    const double steady_start = w1 > w0 ? at(w0).x : 0.0;
+    const double steady_end = w1 > w0 ? at(w1 - 1).y : 0.0;
     const double bs = busy.value();
     const double window = __dadd_rn(last_end, -first_start);
     const double bubble = __dadd_rn(window, -bs);
@@ -692,9 +725,11 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     // coordinates here — in increasing order, so both sums see the
     // reference's terms in the reference's order.
     const int64_t lbase = nb + 2 * (int64_t)S * B + 2 * (int64_t)s * B;
-    Serial<LinkIds> cf{st, en, LinkIds{lbase, 0}, B}, cb{st, en, LinkIds{lbase, 1}, B};
-    Serial<StageIds> u0{st, en, StageIds{nb + 2 * (int64_t)s * B, counts[x], B}, 2 * B};
-    Serial<StageIds> u1{st, en, StageIds{nb + 2 * (int64_t)(s + 1) * B, counts[x + 1], B}, 2 * B};
+    Serial<LinkAt<TRACE>> cf{LinkAt<TRACE>{in, lbase, 0, B}, B};
+    Serial<LinkAt<TRACE>> cb{LinkAt<TRACE>{in, lbase, 1, B}, B};
+    Serial<StageAt<TRACE>> u0{StageAt<TRACE>{in, nb + 2 * (int64_t)s * B, counts[x], B}, 2 * B};
+    Serial<StageAt<TRACE>> u1{
+        StageAt<TRACE>{in, nb + 2 * (int64_t)(s + 1) * B, counts[x + 1], B}, 2 * B};
     cf.init();
     cb.init();
     u0.init();
@@ -743,13 +778,16 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
   const double fn = (double)n;
   const double mx = __ddiv_rn((double)sx, fn);
   PySum sy;
-  for (int i = 2 * K + 1; i <= B; i += K) sy.add(st[nb + 2 * (int64_t)(i - 1)]);
+  // start of F(mb i) on stage 0
+  const StageAt<TRACE> at0{in, nb, K, B};
+  auto f_start = [&](int i) { return at0(encode_op(i, true, K, B)).x; };
+  for (int i = 2 * K + 1; i <= B; i += K) sy.add(f_start(i));
   const double my = __ddiv_rn(sy.value(), fn);
   PySum sxx, sxy;
   for (int i = 2 * K + 1; i <= B; i += K) {
     const double dx = __dadd_rn((double)i, -mx);
     sxx.add(__dmul_rn(dx, dx));  // (x - mean_x) ** 2
-    sxy.add(__dmul_rn(dx, __dadd_rn(st[nb + 2 * (int64_t)(i - 1)], -my)));
+    sxy.add(__dmul_rn(dx, __dadd_rn(f_start(i), -my)));
   }
   steady_rate[p] = __ddiv_rn(sxy.value(), sxx.value());
 }
@@ -788,24 +826,24 @@ extern "C" size_t hapt_sim_workspace_bytes(int64_t total_stages, int32_t ring_de
   return align_up(ts * 2 * ring_depth * 8) + sim_tail_bytes(ts);
 }
 
-extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
-                             const double *t_bwd, const double *comm, const int32_t *counts,
-                             const int32_t *num_mb, double *makespan, double *node_start,
-                             double *node_end, const int64_t *node_off, int32_t ring_depth,
-                             int32_t *status, void *work, size_t work_bytes, void *stream) {
+namespace {
+int sim_1f1b(const char *who, int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
+             const double *t_bwd, const double *comm, const int32_t *counts,
+             const int32_t *num_mb, double *makespan, NodeOut out, int32_t ring_depth,
+             int32_t *status, void *work, size_t work_bytes, void *stream) {
   if (n_plans < 1 || !stage_off || !t_fwd || !t_bwd || !comm || !counts || !num_mb ||
-      !makespan || !status || !work || ring_depth < 2 ||
-      ((node_start != nullptr) != (node_end != nullptr)) || (node_start && !node_off)) {
-    set_error("hapt_sim_1f1b: invalid arguments");
+      !makespan || !status || !work || ring_depth < 2) {
+    set_error("%s: invalid arguments", who);
     return HAPT_EINVAL;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  const bool nodes = out.start || out.trace;
   // total stages = stage_off[n_plans] lives on the device; the caller sized
   // `work` with hapt_sim_workspace_bytes(total_stages, ring_depth), so the
   // ring region is what remains after the tail
   const size_t tail = sim_tail_bytes((size_t)n_plans);
   if (work_bytes < tail + 2 * (size_t)ring_depth * 8) {
-    set_error("hapt_sim_1f1b: workspace too small");
+    set_error("%s: workspace too small", who);
     return HAPT_ENOSPACE;
   }
   double *ring = (double *)work;
@@ -813,11 +851,11 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   int32_t *perm = (int32_t *)wt;
   int32_t *cnt = (int32_t *)(wt + align_up((size_t)n_plans * 4));
   int32_t *bhist = cnt + 32;
-  if (node_start && n_plans < 4096) {  // per-node outputs of a few plans: generic walk
+  if (nodes && n_plans < 4096) {  // per-node outputs of a few plans: generic walk
     k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, nullptr, nullptr, stage_off, t_fwd,
-                                                  t_bwd, comm, counts, num_mb, makespan,
-                                                  node_start, node_end, node_off, ring_depth,
-                                                  ring, status); ::hapt::note_launch();
+                                                  t_bwd, comm, counts, num_mb, makespan, out,
+                                                  ring_depth, ring, status);
+    ::hapt::note_launch();
     HAPT_LAUNCHED("k_sim");
     return HAPT_OK;
   }
@@ -848,7 +886,7 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   if (h[SV] > 0) {                                                                            \
     HAPT_CUDA(cudaStreamWaitEvent(side[SV], ev[0], 0));                                       \
     launch_sim_s<SV>(perm + h[10 + SV], h[SV], stage_off, t_fwd, t_bwd, comm, counts, num_mb, \
-                     makespan, status, node_start, node_end, node_off, side[SV]);             \
+                     makespan, status, out, side[SV]);                                         \
     HAPT_CUDA(cudaEventRecord(ev[SV], side[SV]));                                             \
     HAPT_CUDA(cudaStreamWaitEvent(st, ev[SV], 0));                                            \
   }
@@ -861,17 +899,48 @@ extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const do
   HAPT_CUDA(cudaMemsetAsync(cnt + 20, 0, 4, st));
   if (h[0] > 0) {
     k_sim<<<grid_for(h[0], 128), 128, 0, st>>>(h[0], perm, cnt + 0, stage_off, t_fwd, t_bwd,
-                                               comm, counts, num_mb, makespan, node_start,
-                                               node_end, node_off, ring_depth, ring, status);
+                                               comm, counts, num_mb, makespan, out, ring_depth,
+                                               ring, status);
     ::hapt::note_launch();
   }
   k_sim_retry<<<grid_for(n_plans, 256), 256, 0, st>>>(n_plans, status, perm + h[0], cnt + 20); ::hapt::note_launch();
   k_sim<<<grid_for(n_plans, 128), 128, 0, st>>>(n_plans, perm + h[0], cnt + 20, stage_off,
                                                 t_fwd, t_bwd, comm, counts, num_mb, makespan,
-                                                node_start, node_end, node_off, ring_depth, ring,
-                                                status); ::hapt::note_launch();
+                                                out, ring_depth, ring, status);
+  ::hapt::note_launch();
   HAPT_LAUNCHED("k_sim");
   return HAPT_OK;
+}
+}  // namespace
+
+extern "C" int hapt_sim_1f1b(int32_t n_plans, const int32_t *stage_off, const double *t_fwd,
+                             const double *t_bwd, const double *comm, const int32_t *counts,
+                             const int32_t *num_mb, double *makespan, double *node_start,
+                             double *node_end, const int64_t *node_off, int32_t ring_depth,
+                             int32_t *status, void *work, size_t work_bytes, void *stream) {
+  if (((node_start != nullptr) != (node_end != nullptr)) || (node_start && !node_off)) {
+    set_error("hapt_sim_1f1b: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  return sim_1f1b("hapt_sim_1f1b", n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb,
+                  makespan, NodeOut{node_start, node_end, nullptr, node_off}, ring_depth, status,
+                  work, work_bytes, stream);
+}
+
+extern "C" int hapt_sim_1f1b_trace(int32_t n_plans, const int32_t *stage_off,
+                                   const double *t_fwd, const double *t_bwd, const double *comm,
+                                   const int32_t *counts, const int32_t *num_mb,
+                                   double *makespan, double *trace, const int64_t *trace_off,
+                                   int32_t ring_depth, int32_t *status, void *work,
+                                   size_t work_bytes, void *stream) {
+  if (!trace || !trace_off || ((uintptr_t)trace & 15)) {
+    set_error("hapt_sim_1f1b_trace: invalid arguments (trace must be 16-byte aligned)");
+    return HAPT_EINVAL;
+  }
+  return sim_1f1b("hapt_sim_1f1b_trace", n_plans, stage_off, t_fwd, t_bwd, comm, counts,
+                  num_mb, makespan,
+                  NodeOut{nullptr, nullptr, reinterpret_cast<double2 *>(trace), trace_off},
+                  ring_depth, status, work, work_bytes, stream);
 }
 
 extern "C" size_t hapt_dag_workspace_bytes(int32_t n_nodes) {
@@ -897,6 +966,32 @@ extern "C" int hapt_dag_longest_path(int32_t n_nodes, const int32_t *succ_off,
   return HAPT_OK;
 }
 
+namespace {
+int analyze_1f1b(const char *who, int32_t n_plans, int32_t total_stages,
+                 const int32_t *stage_off, const double *t_fwd, const double *t_bwd,
+                 const double *comm, const int32_t *counts, const int32_t *num_mb,
+                 const double *mem_act, NodeIn in, const int32_t *status, double *stage_rep,
+                 int32_t *peak_inflight, double *link_rep, double *steady_rate, void *stream) {
+  if (n_plans < 1 || total_stages < 1 || !stage_off || !t_fwd || !t_bwd || !comm || !counts ||
+      !num_mb || !in.off || !stage_rep || !peak_inflight || !link_rep || !steady_rate) {
+    set_error("%s: invalid arguments", who);
+    return HAPT_EINVAL;
+  }
+  const unsigned grid = grid_for(2 * (size_t)total_stages + n_plans, 128);
+  if (in.trace)
+    k_analyze<true><<<grid, 128, 0, (cudaStream_t)stream>>>(
+        n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb, mem_act, in, status, stage_rep,
+        peak_inflight, link_rep, steady_rate);
+  else
+    k_analyze<false><<<grid, 128, 0, (cudaStream_t)stream>>>(
+        n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb, mem_act, in, status, stage_rep,
+        peak_inflight, link_rep, steady_rate);
+  ::hapt::note_launch();
+  HAPT_LAUNCHED("k_analyze");
+  return HAPT_OK;
+}
+}  // namespace
+
 extern "C" int hapt_analyze_1f1b(int32_t n_plans, int32_t total_stages, const int32_t *stage_off,
                                  const double *t_fwd, const double *t_bwd, const double *comm,
                                  const int32_t *counts, const int32_t *num_mb,
@@ -905,16 +1000,30 @@ extern "C" int hapt_analyze_1f1b(int32_t n_plans, int32_t total_stages, const in
                                  const int32_t *status, double *stage_rep,
                                  int32_t *peak_inflight, double *link_rep, double *steady_rate,
                                  void *stream) {
-  if (n_plans < 1 || total_stages < 1 || !stage_off || !t_fwd || !t_bwd || !comm || !counts ||
-      !num_mb || !node_start || !node_end || !node_off || !stage_rep || !peak_inflight ||
-      !link_rep || !steady_rate) {
+  if (!node_start || !node_end) {
     set_error("hapt_analyze_1f1b: invalid arguments");
     return HAPT_EINVAL;
   }
-  k_analyze<<<grid_for(2 * (size_t)total_stages + n_plans, 128), 128, 0, (cudaStream_t)stream>>>(
-      n_plans, stage_off, t_fwd, t_bwd, comm, counts, num_mb, mem_act, node_start, node_end,
-      node_off, status, stage_rep, peak_inflight, link_rep, steady_rate);
-  ::hapt::note_launch();
-  HAPT_LAUNCHED("k_analyze");
-  return HAPT_OK;
+  return analyze_1f1b("hapt_analyze_1f1b", n_plans, total_stages, stage_off, t_fwd, t_bwd, comm,
+                      counts, num_mb, mem_act, NodeIn{node_start, node_end, nullptr, node_off},
+                      status, stage_rep, peak_inflight, link_rep, steady_rate, stream);
+}
+
+extern "C" int hapt_analyze_1f1b_trace(int32_t n_plans, int32_t total_stages,
+                                       const int32_t *stage_off, const double *t_fwd,
+                                       const double *t_bwd, const double *comm,
+                                       const int32_t *counts, const int32_t *num_mb,
+                                       const double *mem_act, const double *trace,
+                                       const int64_t *trace_off, const int32_t *status,
+                                       double *stage_rep, int32_t *peak_inflight,
+                                       double *link_rep, double *steady_rate, void *stream) {
+  if (!trace || ((uintptr_t)trace & 15)) {
+    set_error("hapt_analyze_1f1b_trace: invalid arguments (trace must be 16-byte aligned)");
+    return HAPT_EINVAL;
+  }
+  return analyze_1f1b("hapt_analyze_1f1b_trace", n_plans, total_stages, stage_off, t_fwd, t_bwd,
+                      comm, counts, num_mb, mem_act,
+                      NodeIn{nullptr, nullptr, reinterpret_cast<const double2 *>(trace),
+                             trace_off},
+                      status, stage_rep, peak_inflight, link_rep, steady_rate, stream);
 }

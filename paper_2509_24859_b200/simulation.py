@@ -412,8 +412,9 @@ class PlanBatch:
         (SURVEY.md §8(f)2): per plan the reference's SimulationReport, as
         packed device arrays.  Plans are processed in chunks whose traces
         (16 B per DAG node: start and end) fit `max_node_bytes`; each chunk is
-        one hapt_sim_1f1b launch writing node times and one hapt_analyze_1f1b
-        launch reading them back."""
+        one hapt_sim_1f1b_trace launch writing node times (trace layout: each
+        stage's ops in program order, so stores fill whole sectors) and one
+        hapt_analyze_1f1b_trace launch reading them back."""
         import torch
 
         from . import _lib
@@ -436,7 +437,7 @@ class PlanBatch:
                 raise SimulationError("mem_act must hold one value per packed stage")
         so = self.stage_off_host
         sc = np.diff(so)
-        nodes = mb_host * (4 * sc - 2) + 1  # B(4S-2)+1 per plan (simulation.py:103-111)
+        nodes = mb_host * (4 * sc - 2)  # B(4S-2) per plan + the sink (simulation.py:103-111)
         rep = BatchReport(
             stage_off=self.stage_off,
             makespan=torch.empty(P, dtype=torch.float64, device=dev),
@@ -458,20 +459,19 @@ class PlanBatch:
             noff = torch.zeros(p1 - p0, dtype=torch.int64, device=dev)
             if p1 - p0 > 1:
                 noff[1:] = torch.from_numpy(np.cumsum(nodes[p0:p1 - 1])).to(dev)
-            start = torch.empty(n, dtype=torch.float64, device=dev)
-            end = torch.empty(n, dtype=torch.float64, device=dev)
+            trace = torch.empty(2 * max(n, 1), dtype=torch.float64, device=dev)
             nb = lib.hapt_sim_workspace_bytes(s1 - s0, ring)
             ws = _sim_ws(dev, nb)
             sl = lambda t: t[s0:s1]  # noqa: E731
-            check(lib.hapt_sim_1f1b(
+            check(lib.hapt_sim_1f1b_trace(
                 p1 - p0, off.data_ptr(), ptr(sl(self.t_fwd)), ptr(sl(self.t_bwd)),
                 ptr(sl(self.comm)), ptr(sl(counts)), ptr(mb[p0:p1]), ptr(rep.makespan[p0:p1]),
-                start.data_ptr(), end.data_ptr(), noff.data_ptr(), ring,
-                ptr(rep.status[p0:p1]), ws.data_ptr(), nb, stream_ptr()))
-            check(lib.hapt_analyze_1f1b(
+                trace.data_ptr(), noff.data_ptr(), ring, ptr(rep.status[p0:p1]),
+                ws.data_ptr(), nb, stream_ptr()))
+            check(lib.hapt_analyze_1f1b_trace(
                 p1 - p0, s1 - s0, off.data_ptr(), ptr(sl(self.t_fwd)), ptr(sl(self.t_bwd)),
                 ptr(sl(self.comm)), ptr(sl(counts)), ptr(mb[p0:p1]),
-                0 if mem is None else ptr(sl(mem)), start.data_ptr(), end.data_ptr(),
+                0 if mem is None else ptr(sl(mem)), trace.data_ptr(),
                 noff.data_ptr(), ptr(rep.status[p0:p1]), ptr(rep.stage[s0:s1]),
                 ptr(rep.peak_inflight[s0:s1]), ptr(rep.link[s0:s1]),
                 ptr(rep.steady_rate[p0:p1]), stream_ptr()))

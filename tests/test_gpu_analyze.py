@@ -141,3 +141,82 @@ def test_analyze_large_batch_fast_path():
     tf, tb, cm, cn, B, mem, sc = dense(plans)
     rep = analyze_batch(tf, tb, cm, cn, B, mem_act=mem, stage_counts=sc)
     check_against_goldens(rep, plans)
+
+
+@pytest.mark.parametrize("copies", [1, 11])  # generic walk / bucketed per-S kernels
+def test_both_node_layouts_through_the_abi(copies):
+    """hapt_sim_1f1b (reference node numbering) + hapt_analyze_1f1b give the
+    goldens too, and hapt_sim_1f1b_trace's pairs are the same node times in
+    the trace order the header documents."""
+    import torch
+
+    from paper_2509_24859_b200 import _lib
+    from paper_2509_24859_b200._lib import check, ptr, stream_ptr
+    from paper_2509_24859_b200.simulation import BatchReport, PlanBatch, _sim_ws
+
+    plans = load() * copies
+    tf, tb, cm, cn, B, mem, sc = dense(plans)
+    pb = PlanBatch(tf, tb, cm, stage_counts=sc)
+    dev = pb.device
+    mask = np.arange(tf.shape[1])[None, :] < sc[:, None]
+    counts = torch.as_tensor(cn[mask], dtype=torch.int32, device=dev)
+    memd = torch.as_tensor(mem[mask], dtype=torch.float64, device=dev)
+    mb = torch.as_tensor(B, dtype=torch.int32, device=dev)
+    P, TS = pb.n_plans, pb.total_stages
+    ref_nodes = B.astype(np.int64) * (4 * sc - 2) + 1
+    tr_pairs = B.astype(np.int64) * (4 * sc - 2)
+    roff = torch.as_tensor(np.concatenate([[0], np.cumsum(ref_nodes)[:-1]]), device=dev)
+    toff = torch.as_tensor(np.concatenate([[0], np.cumsum(tr_pairs)[:-1]]), device=dev)
+    start = torch.empty(int(ref_nodes.sum()), dtype=torch.float64, device=dev)
+    end = torch.empty_like(start)
+    trace = torch.empty(2 * int(tr_pairs.sum()), dtype=torch.float64, device=dev)
+    ring = int(counts.max().item()) + 2
+    lib = _lib.lib()
+    nb = lib.hapt_sim_workspace_bytes(TS, ring)
+    ws = _sim_ws(dev, nb)
+
+    def report():
+        return BatchReport(
+            stage_off=pb.stage_off,
+            makespan=torch.empty(P, dtype=torch.float64, device=dev),
+            status=torch.empty(P, dtype=torch.int32, device=dev),
+            stage=torch.empty(TS, 6, dtype=torch.float64, device=dev),
+            peak_inflight=torch.empty(TS, dtype=torch.int32, device=dev),
+            link=torch.empty(TS, 3, dtype=torch.float64, device=dev),
+            steady_rate=torch.empty(P, dtype=torch.float64, device=dev))
+
+    common = (pb.stage_off.data_ptr(), ptr(pb.t_fwd), ptr(pb.t_bwd), ptr(pb.comm), ptr(counts),
+              ptr(mb))
+    ra, rb = report(), report()
+    check(lib.hapt_sim_1f1b(P, *common, ptr(ra.makespan), ptr(start), ptr(end), ptr(roff), ring,
+                            ptr(ra.status), ws.data_ptr(), nb, stream_ptr()))
+    check(lib.hapt_analyze_1f1b(P, TS, *common, ptr(memd), ptr(start), ptr(end), ptr(roff),
+                                ptr(ra.status), ptr(ra.stage), ptr(ra.peak_inflight),
+                                ptr(ra.link), ptr(ra.steady_rate), stream_ptr()))
+    check(lib.hapt_sim_1f1b_trace(P, *common, ptr(rb.makespan), ptr(trace), ptr(toff), ring,
+                                  ptr(rb.status), ws.data_ptr(), nb, stream_ptr()))
+    check(lib.hapt_analyze_1f1b_trace(P, TS, *common, ptr(memd), ptr(trace), ptr(toff),
+                                      ptr(rb.status), ptr(rb.stage), ptr(rb.peak_inflight),
+                                      ptr(rb.link), ptr(rb.steady_rate), stream_ptr()))
+    check_against_goldens(ra, plans)
+    check_against_goldens(rb, plans)
+    # trace pairs vs reference-numbered nodes, for a few plans
+    from paper_2509_24859_b200.scheduling import FWD, build_program
+
+    st_h, en_h, tr_h = start.cpu().numpy(), end.cpu().numpy(), trace.cpu().numpy()
+    for i in range(0, len(plans), max(1, len(plans) // 25)):
+        p, S, Bi = plans[i], int(sc[i]), int(B[i])
+        prog = build_program(_counts(p), Bi)
+        r0, t0 = int(roff[i]), 2 * int(toff[i])
+        want = []
+        for s in range(S):
+            for kind, m in prog.stages[s].ops:
+                j = r0 + 2 * (s * Bi + m - 1) + (0 if kind == FWD else 1)
+                want.append((st_h[j], en_h[j]))
+        for l in range(S - 1):
+            for d in (0, 1):
+                for m in range(1, Bi + 1):
+                    j = r0 + 2 * S * Bi + 2 * (l * Bi + m - 1) + d
+                    want.append((st_h[j], en_h[j]))
+        got = tr_h[t0:t0 + 2 * len(want)].reshape(-1, 2)
+        assert np.array_equal(got, np.array(want)), i

@@ -1,5 +1,6 @@
 """Split of PlanBatch.analyze time: simulation with node times vs the report
-kernel, on config-E plans (B = 128).
+kernel, on config-E plans (B = 128), in both node layouts (reference
+numbering; trace layout, which PlanBatch.analyze uses).
 
     python tools/time_analyze.py [--plans 100000]
 """
@@ -38,6 +39,10 @@ def main():
     n = int(nodes.sum())
     start = torch.empty(n, dtype=torch.float64, device=dev)
     end = torch.empty(n, dtype=torch.float64, device=dev)
+    tpairs = B * (4 * sc - 2)
+    toff = torch.zeros(P, dtype=torch.int64, device=dev)
+    toff[1:] = torch.from_numpy(np.cumsum(tpairs[:-1])).to(dev)
+    trace = torch.empty(2 * int(tpairs.sum()), dtype=torch.float64, device=dev)
     ring = int(counts.max().item()) + 2
     nb = lib.hapt_sim_workspace_bytes(TS, ring)
     ws = _sim_ws(dev, nb)
@@ -60,7 +65,20 @@ def main():
                                     ptr(start), ptr(end), ptr(noff), ptr(status), ptr(stage),
                                     ptr(peak), ptr(link), ptr(rate), stream_ptr()))
 
-    for name, fn in (("sim+nodes", sim), ("analyze", rep)):
+    def sim_t():
+        check(lib.hapt_sim_1f1b_trace(P, pb.stage_off.data_ptr(), ptr(pb.t_fwd), ptr(pb.t_bwd),
+                                      ptr(pb.comm), ptr(counts), ptr(mb), ptr(mk), ptr(trace),
+                                      ptr(toff), ring, ptr(status), ws.data_ptr(), nb,
+                                      stream_ptr()))
+
+    def rep_t():
+        check(lib.hapt_analyze_1f1b_trace(P, TS, pb.stage_off.data_ptr(), ptr(pb.t_fwd),
+                                          ptr(pb.t_bwd), ptr(pb.comm), ptr(counts), ptr(mb), 0,
+                                          ptr(trace), ptr(toff), ptr(status), ptr(stage),
+                                          ptr(peak), ptr(link), ptr(rate), stream_ptr()))
+
+    for name, fn in (("sim+nodes", sim), ("analyze", rep), ("sim+trace", sim_t),
+                     ("analyze/tr", rep_t)):
         fn()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

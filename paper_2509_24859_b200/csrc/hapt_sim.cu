@@ -123,15 +123,22 @@ __device__ __forceinline__ int encode_op(int mb, bool isF, int N, int B) {
 //     thread writes each of its lists front to back, so every 32-byte sector
 //     is complete after two consecutive stores instead of collecting four
 //     scattered ones (partial sectors evicted from L2 cost a DRAM read).
-// nb = off[p] in either layout.
+// nb = off[p] in either layout.  Kernels that know the layout at compile
+// time pass it as M (kRefNodes / kTrace); M = -1 decides at run time.
+constexpr int kNoNodes = 0, kRefNodes = 1, kTrace = 2;
+
 struct NodeOut {
   double *start, *end;
   double2 *trace;
   const int64_t *off;
+  __host__ __device__ int mode() const {
+    return trace ? kTrace : start ? kRefNodes : kNoNodes;
+  }
   __device__ bool on() const { return start != nullptr || trace != nullptr; }
+  template <int M = -1>
   __device__ void op(int64_t nb, int B, int s, int mb, bool isF, int q, double a,
                      double e) const {
-    if (trace) {
+    if (M < 0 ? trace != nullptr : M == kTrace) {
       trace[nb + 2 * (int64_t)s * B + q] = make_double2(a, e);
     } else {
       const int64_t id = nb + 2 * ((int64_t)s * B + (mb - 1)) + (isF ? 0 : 1);
@@ -139,10 +146,11 @@ struct NodeOut {
       end[id] = e;
     }
   }
+  template <int M = -1>
   __device__ void xfer(int64_t nb, int S, int B, int l, int dir, int mb, double a,
                        double e) const {
     const int64_t base = nb + 2 * (int64_t)S * B + 2 * (int64_t)l * B;
-    if (trace) {
+    if (M < 0 ? trace != nullptr : M == kTrace) {
       trace[base + (int64_t)dir * B + (mb - 1)] = make_double2(a, e);
     } else {
       const int64_t id = base + 2 * (int64_t)(mb - 1) + dir;
@@ -150,8 +158,9 @@ struct NodeOut {
       end[id] = e;
     }
   }
+  template <int M = -1>
   __device__ void sink(int64_t nb, int S, int B, double mk) const {
-    if (trace) return;
+    if (M < 0 ? trace != nullptr : M == kTrace) return;
     const int64_t id = nb + 2 * (int64_t)S * B + 2 * (int64_t)(S - 1) * B;
     start[id] = mk;
     end[id] = mk;
@@ -347,7 +356,7 @@ struct SimCfg {
   static constexpr size_t smem = (size_t)(S > 1 ? S - 1 : 1) * 2 * kRing * threads * 8;
 };
 
-template <int S>
+template <int S, int M>  // M: kNoNodes / kRefNodes / kTrace
 __global__ void __launch_bounds__(SimCfg<S>::threads)
     k_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
             const double *t_bwd, const double *comm, const int32_t *counts,
@@ -386,7 +395,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
   }
   double mk = 0.0;
   // optional per-node times in the reference numbering (simulation.py:103-111)
-  const bool nodes = out.on();
+  constexpr bool nodes = M != kNoNodes;
   const int64_t nb = nodes ? out.off[p] : 0;
   int remaining = S;
   while (remaining > 0) {
@@ -409,7 +418,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
           const double en = __dadd_rn(st, isF ? tf[s] : tb[s]);
           prev[s] = en;
           mk = fmax(mk, en);
-          if (nodes) out.op(nb, B, s, mb, isF, pos[s], st, en);
+          if (nodes) out.op<M>(nb, B, s, mb, isF, pos[s], st, en);
           if (isF) {
             fd[s] = mb;
             if (s < S - 1) {  // forward transfer on link s (simulation.py:130-140)
@@ -418,7 +427,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
               lcf[s] = ce;
               mk = fmax(mk, ce);
               slot(s, 0, mb) = ce;
-              if (nodes) out.xfer(nb, S, B, s, 0, mb, cs, ce);
+              if (nodes) out.xfer<M>(nb, S, B, s, 0, mb, cs, ce);
             }
           } else {
             bd[s] = mb;
@@ -428,7 +437,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
               lcb[s - 1] = ce;
               mk = fmax(mk, ce);
               slot(s - 1, 1, mb) = ce;
-              if (nodes) out.xfer(nb, S, B, s - 1, 1, mb, cs, ce);
+              if (nodes) out.xfer<M>(nb, S, B, s - 1, 1, mb, cs, ce);
             }
           }
           if (++pos[s] == 2 * B) --remaining;
@@ -441,7 +450,7 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
       return;
     }
   }
-  if (nodes) out.sink(nb, S, B, mk);
+  if (nodes) out.sink<M>(nb, S, B, mk);
   makespan[p] = mk;
   status[p] = HAPT_OK;
 }
@@ -514,11 +523,25 @@ void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const do
   using C = SimCfg<S>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sim_s<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem);
+    cudaFuncSetAttribute(k_sim_s<S, kNoNodes>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::smem);
+    cudaFuncSetAttribute(k_sim_s<S, kRefNodes>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::smem);
+    cudaFuncSetAttribute(k_sim_s<S, kTrace>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::smem);
     attr = true;
   }
-  k_sim_s<S><<<grid_for(n, C::threads), C::threads, C::smem, st>>>(
-      perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, out);
+  const unsigned grid = grid_for(n, C::threads);
+  const int m = out.mode();
+  if (m == kTrace)
+    k_sim_s<S, kTrace><<<grid, C::threads, C::smem, st>>>(
+        perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, out);
+  else if (m == kRefNodes)
+    k_sim_s<S, kRefNodes><<<grid, C::threads, C::smem, st>>>(
+        perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, out);
+  else
+    k_sim_s<S, kNoNodes><<<grid, C::threads, C::smem, st>>>(
+        perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, out);
   ::hapt::note_launch();
 }
 

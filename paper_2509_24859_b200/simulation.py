@@ -407,7 +407,7 @@ class PlanBatch:
         return mk, status
 
     def analyze(self, counts, num_microbatches, mem_act=None,
-                max_node_bytes: int = 2 << 30) -> "BatchReport":
+                max_node_bytes: int = 4 << 30) -> "BatchReport":
         """simulate + analyze + steady_state_rate(stage=1) of every plan
         (SURVEY.md §8(f)2): per plan the reference's SimulationReport, as
         packed device arrays.  Plans are processed in chunks whose traces
@@ -448,12 +448,11 @@ class PlanBatch:
             steady_rate=torch.empty(P, dtype=torch.float64, device=dev))
         ring = int(counts.max().item()) + 2
         cap = max(1, int(max_node_bytes) // 16)
+        cum = np.concatenate([[0], np.cumsum(nodes)])  # chunk = longest run within cap
         p0 = 0
         while p0 < P:
-            p1, n = p0, 0
-            while p1 < P and (p1 == p0 or n + nodes[p1] <= cap):
-                n += int(nodes[p1])
-                p1 += 1
+            p1 = max(p0 + 1, int(np.searchsorted(cum, cum[p0] + cap, side="right")) - 1)
+            n = int(cum[p1] - cum[p0])
             s0, s1 = int(so[p0]), int(so[p1])
             off = (self.stage_off[p0:p1 + 1] - s0).contiguous()
             noff = torch.zeros(p1 - p0, dtype=torch.int64, device=dev)

@@ -207,16 +207,19 @@ class SweepResult:
     ftop: np.ndarray | None = None     # F[s,1,G] per candidate [n][s_max+1] (keep_ftop)
 
 
-_WS_CACHE: dict = {}  # device -> scratch tensor reused by every Sweeper
+_WS_CACHE: dict = {}  # (device, stream) -> scratch tensor reused by every Sweeper
 _FREE_MEM: dict = {}
 
 
 def _scratch(device: torch.device, nbytes: int) -> torch.Tensor:
-    buf = _WS_CACHE.get(device)
+    """Scratch shared by every sweep issued on the current stream (work on one
+    stream is ordered, so reuse is safe; other streams get their own)."""
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    buf = _WS_CACHE.get(key)
     if buf is None or buf.numel() < nbytes:
-        _WS_CACHE.pop(device, None)
+        _WS_CACHE.pop(key, None)
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        _WS_CACHE[device] = buf
+        _WS_CACHE[key] = buf
     return buf
 
 

@@ -523,11 +523,12 @@ _SIM_WS: dict = {}
 def _sim_ws(device, nbytes):
     import torch
 
-    buf = _SIM_WS.get(device)
+    key = (device, torch.cuda.current_stream(device).cuda_stream)  # one per stream
+    buf = _SIM_WS.get(key)
     if buf is None or buf.numel() < nbytes:
-        _SIM_WS.pop(device, None)
+        _SIM_WS.pop(key, None)
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        _SIM_WS[device] = buf
+        _SIM_WS[key] = buf
     return buf
 
 

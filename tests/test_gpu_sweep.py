@@ -30,15 +30,17 @@ def ops_builder(name):
     return lambda mb: llama_like_ops(b=mb)
 
 
+@pytest.mark.parametrize("concurrent", [True, False])
 @pytest.mark.parametrize("name", ["A", "D1"])
-def test_microbatch_sweep_equals_reference(name):
+def test_microbatch_sweep_equals_reference(name, concurrent):
     from paper_2509_24859_b200.sweep import best_point, microbatch_sweep
 
     recs = golden()[name]
     _, cluster, model, rho, _, eps = to_types(load_json(name))
     points = [(r["mb"], r["B"]) for r in recs]
     res = microbatch_sweep(ops_builder(name), cluster, points, model=model,
-                           imbalance_ratio=rho, epsilon=eps, batch_size=4)
+                           imbalance_ratio=rho, epsilon=eps, batch_size=4,
+                           concurrent=concurrent)
     for pt, r in zip(res, recs):
         assert (pt.mb_size, pt.num_microbatches) == (r["mb"], r["B"])
         assert [l.flops for l in pt.layers.layers] == r["flops"]

@@ -54,8 +54,13 @@ int cpl_for(const hapt_tables *t, int n_cand) {
     const int v = atoi(e);
     if (v == 1 || v == 2 || v == 4) return v;
   }
+  // two candidates per lane halve the warps a layer needs but lengthen each
+  // warp's chain; measured (tools/time_batch.py, D1 and C) they pay off once
+  // a batch has more than ~240 candidates (7.5 groups of 32) on tables large
+  // enough to fill the GPU -- below that the extra warps of CPL = 1 hide more
+  // latency (D1: 16 candidates 2.55 -> 1.82 ms, 224 candidates 4.13 -> 3.79 ms)
   const long warps2 = (long)t->L * t->G * ((n_cand + 63) / 64);
-  return warps2 >= 16384 ? 2 : 1;
+  return (warps2 >= 16384 && n_cand > 240) ? 2 : 1;
 }
 
 #ifndef HAPT_U4

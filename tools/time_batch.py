@@ -1,6 +1,7 @@
 """Device time vs wall time of one candidate batch (the search's unit of work).
 
     python tools/time_batch.py [--config D1] [--sizes 1,38,117,256]
+    python tools/time_batch.py --shards 1,2,4,8   # rank 0's share pool[0::W]
 """
 import argparse
 import os
@@ -15,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="D1")
     ap.add_argument("--sizes", default="1,38,117,256")
+    ap.add_argument("--shards", default="", help="time pool[0::W] for each W instead")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -28,8 +30,13 @@ def main():
     tables = DpTables(store, boundary_costs(layers, cluster))
     pool = np.asarray(store.feasible_t_values())
     sw = tables.sweeper
-    for n in (int(x) for x in args.sizes.split(",")):
-        idx = np.linspace(len(pool) // 3, len(pool) - 1, n).astype(int)
+    if args.shards:
+        batches = [np.arange(0, len(pool), int(w)) for w in args.shards.split(",")]
+    else:
+        batches = [np.linspace(len(pool) // 3, len(pool) - 1, int(n)).astype(int)
+                   for n in args.sizes.split(",")]
+    for idx in batches:
+        n = len(idx)
         tm = torch.from_numpy(pool[idx]).cuda()
         for _ in range(3):
             sw.sweep_device(tm)

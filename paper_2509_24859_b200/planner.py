@@ -264,8 +264,12 @@ class CandidateEvaluator:
         keep_bp: record the batch's backpointers (within BP_BUDGET) so a
         winner from it is walked instead of re-swept -- worth it only for a
         batch that can contain the final winner."""
-        todo = sorted({int(i) for i in indices if not self.known(int(i))})
-        if not todo:
+        if isinstance(indices, range):
+            idx = np.arange(indices.start, indices.stop, indices.step, dtype=np.int64)
+        else:
+            idx = np.unique(np.fromiter((int(i) for i in indices), dtype=np.int64))
+        todo = idx[self.best_s[idx] == -2]  # sorted, unique, not yet known
+        if not len(todo):
             return
         self.batches += 1
         self.evaluated += len(todo)
@@ -282,7 +286,7 @@ class CandidateEvaluator:
             self.states[todo] = res.states
             if res.bp is not None:
                 self._bp_bytes += need
-                for pos, i in enumerate(todo):
+                for pos, i in enumerate(todo.tolist()):
                     self._bp_of[i] = (res, pos)
         elif self.ftop is not None:
             ts, bs, st, ft = self.dist.evaluate_sharded(self.tables.sweeper, self.pool, todo,

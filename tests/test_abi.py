@@ -65,3 +65,28 @@ def test_product_does_not_import_oracle():
                 text = open(os.path.join(root, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "import meshpipe" not in text and "from meshpipe" not in text, f
+
+
+def test_trace_entry_points_validate_arguments():
+    """The trace-layout K3 entry points reject a missing or misaligned trace
+    (argument checks run before any CUDA call, so this runs on CPU)."""
+    import ctypes
+
+    from paper_2509_24859_b200 import _lib, build
+
+    h = _lib.load(build.build())
+    h.hapt_last_error.restype = ctypes.c_char_p
+    one = (ctypes.c_int32 * 4)(0, 1, 1, 1)
+    dbl = (ctypes.c_double * 8)()
+    off = (ctypes.c_int64 * 2)()
+    odd = ctypes.addressof(dbl) + 8  # 8-byte aligned, not 16
+    einval = 1
+    rc = h.hapt_sim_1f1b_trace(1, one, dbl, dbl, dbl, one, one, dbl, None, off, 4, one, dbl,
+                               ctypes.c_size_t(64), None)
+    assert rc == einval and b"hapt_sim_1f1b_trace" in h.hapt_last_error()
+    rc = h.hapt_sim_1f1b_trace(1, one, dbl, dbl, dbl, one, one, dbl, ctypes.c_void_p(odd), off,
+                               4, one, dbl, ctypes.c_size_t(64), None)
+    assert rc == einval and b"16-byte" in h.hapt_last_error()
+    rc = h.hapt_analyze_1f1b_trace(1, 1, one, dbl, dbl, dbl, one, one, None,
+                                   ctypes.c_void_p(odd), off, None, dbl, one, dbl, dbl, None)
+    assert rc == einval and b"hapt_analyze_1f1b_trace" in h.hapt_last_error()

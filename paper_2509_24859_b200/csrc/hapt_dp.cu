@@ -112,6 +112,7 @@ struct Batch {
   int n_opts;
   double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
+  double *Hmin[2];     // [n_groups][G+1][L+1]: min of H over the group's lanes
   double *ftop;
   unsigned long long *states;
   hapt_dp_full full;
@@ -119,7 +120,7 @@ struct Batch {
 
 struct WsLayout {
   size_t tmax_pad, tcnt, cut_sr, kc, ir[3], maxlen, clist, gtot, goff, ticket, gmeta, spart, H0,
-      H1, K0, K1, total;
+      H1, K0, K1, Hm0, Hm1, total;
 };
 
 WsLayout ws_layout(const hapt_tables *t, int n_cand) {
@@ -148,6 +149,8 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   w.H1 = cur; cur += align_up(ng * hg * cw * 8);
   w.K0 = cur; cur += align_up(ng * hg * cw * 2);
   w.K1 = cur; cur += align_up(ng * hg * cw * 2);
+  w.Hm0 = cur; cur += align_up(ng * hg * 8);
+  w.Hm1 = cur; cur += align_up(ng * hg * 8);
   w.total = cur;
   return w;
 }
@@ -254,6 +257,12 @@ __global__ void dp_prep(Batch b) {
       H[e] = __dadd_rn(c2, 0.0);
       K[e] = (uint16_t)((int)ceil(__ddiv_rn(c2, tm)) + 1);
     }
+  }
+  if (threadIdx.x == 0) {  // its lane minimum: finite iff some lane accepts c
+    const double c = b.cb[(size_t)b.g_crow[0] * (b.L + 1) + b.L];
+    bool any = false;
+    for (int j = 0; j < cw; ++j) any |= c <= b.tmax_pad[group * cw + j];
+    b.Hmin[0][(size_t)group * b.hg + b.L] = any ? __dadd_rn(__dmul_rn(2.0, c), 0.0) : kInf;
   }
 }
 
@@ -523,8 +532,19 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     const int T = __shfl_sync(0xffffffffu, incl, 31);
     const int start = incl - len;
     const bool anykk = __any_sync(0xffffffffu, needkk);
+    const double *Hm = b.Hmin[(s - 1) & 1] + gbase;
     for (int r0 = 0; r0 < T; r0 += 32) {
       const int t = r0 + lane;
+      // A transition's value tt + H[lane] (H = 2c + F >= 0) is at least
+      // tt + min over the group's lanes of H, and an update needs a strict
+      // improvement; an entry with tt + Hmin >= every lane's current best
+      // cannot change any lane's winner and is not staged (bv only falls,
+      // so the bound taken here holds for the whole chunk).
+      double bmax = 0.0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) bmax = fmax(bmax, bv[c]);
+#pragma unroll
+      for (int off = 16; off; off >>= 1) bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, off));
       // owner row: number of rows whose entries end at or before t, by binary
       // search over the lanes' inclusive ends (non-decreasing; rows past nch
       // end at T > t for every real entry)
@@ -540,17 +560,29 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       const int oh = __shfl_sync(0xffffffffu, hbase, jj);
       int4 se = make_int4(0, 0, -1, 0);  // inert padding entry
       uint16_t sk = 0;
+      bool keep = false;
       if (t < T) {
         const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
+        const int succ = oh + (x.w & 0xffff);
+        const double tt = __hiloint2double(x.y, x.x);
+        keep = __dadd_rn(tt, __ldg(Hm + succ)) < bmax;
         const unsigned w2 =
             x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
-        se = make_int4(x.x, x.y, (int)w2, (oh + (x.w & 0xffff)) * (256 * CPL));
+        se = make_int4(x.x, x.y, (int)w2, succ * (256 * CPL));
         sk = (uint16_t)((unsigned)x.w >> 16);
       }
-      stage_e[lane] = se;
-      stage_k[lane] = sk;
+      // kept entries first, in order; the rest of the stage is inert
+      const unsigned kept = __ballot_sync(0xffffffffu, keep);
+      const unsigned below = kept & ((1u << lane) - 1u);
+      const int n = __popc(kept);
+      if (keep) {
+        stage_e[__popc(below)] = se;
+        stage_k[__popc(below)] = sk;
+      } else {
+        stage_e[n + (lane - __popc(below))] = make_int4(0, 0, -1, 0);
+        stage_k[n + (lane - __popc(below))] = 0;
+      }
       __syncwarp();
-      const int n = min(32, T - r0);
       if (anykk)
         relax_entries<true, CPL>(stage_e, stage_k, n, cnt2, Hb, Kb, bv, bw2, bw3);
       else
@@ -605,12 +637,17 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   }
   const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
   bool anyfin = false;
+  double hmin = kInf;
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     b.H[s & 1][o_idx + c] = hn[c];
     b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
     anyfin |= hn[c] != kInf;
+    hmin = fmin(hmin, hn[c]);
   }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) hmin = fmin(hmin, __shfl_xor_sync(0xffffffffu, hmin, off));
+  if (lane == 0) b.Hmin[s & 1][gbase + (size_t)g * (L + 1) + (k - 1)] = hmin;
   if (__any_sync(0xffffffffu, anyfin) && lane == 0) {
     int2 *fr = &b.irange[s % 3][(size_t)group * (G + 1) + g];
     atomicMin(&fr->x, k - 1);
@@ -957,6 +994,8 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.H[1] = (double *)(wb + w.H1);
   b.K[0] = (uint16_t *)(wb + w.K0);
   b.K[1] = (uint16_t *)(wb + w.K1);
+  b.Hmin[0] = (double *)(wb + w.Hm0);
+  b.Hmin[1] = (double *)(wb + w.Hm1);
   b.ftop = ftop;
   b.states = (unsigned long long *)states;
   if (full) b.full = *full;

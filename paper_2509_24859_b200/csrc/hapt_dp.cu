@@ -112,7 +112,7 @@ struct Batch {
   int n_opts;
   double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
-  double *Hmin[2];     // [n_groups][G+1][L+1]: min of H over the group's lanes
+  double *Hmin[2];     // [n_groups][G+1][L+1]: lower bound of H over the group's lanes
   double *ftop;
   unsigned long long *states;
   hapt_dp_full full;
@@ -536,15 +536,17 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     for (int r0 = 0; r0 < T; r0 += 32) {
       const int t = r0 + lane;
       // A transition's value tt + H[lane] (H = 2c + F >= 0) is at least
-      // tt + min over the group's lanes of H, and an update needs a strict
+      // tt + Hmin (a lower bound of H over the group's lanes), and an update needs a strict
       // improvement; an entry with tt + Hmin >= every lane's current best
       // cannot change any lane's winner and is not staged (bv only falls,
       // so the bound taken here holds for the whole chunk).
-      double bmax = 0.0;
+      // max over lanes via the high words (non-negative doubles order like
+      // their bit patterns): hi:ffffffff bounds every best from above
+      unsigned mh = 0;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) bmax = fmax(bmax, bv[c]);
-#pragma unroll
-      for (int off = 16; off; off >>= 1) bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, off));
+      for (int c = 0; c < CPL; ++c) mh = max(mh, (unsigned)__double2hiint(bv[c]));
+      mh = __reduce_max_sync(0xffffffffu, mh);
+      const double bmax = mh >= 0x7ff00000u ? kInf : __hiloint2double((int)mh, -1);
       // owner row: number of rows whose entries end at or before t, by binary
       // search over the lanes' inclusive ends (non-decreasing; rows past nch
       // end at T > t for every real entry)
@@ -637,17 +639,16 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   }
   const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
   bool anyfin = false;
-  double hmin = kInf;
+  unsigned hh = 0xffffffffu;  // min over lanes of the high words; hi:0 bounds every H below
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     b.H[s & 1][o_idx + c] = hn[c];
     b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
     anyfin |= hn[c] != kInf;
-    hmin = fmin(hmin, hn[c]);
+    hh = min(hh, (unsigned)__double2hiint(hn[c]));
   }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) hmin = fmin(hmin, __shfl_xor_sync(0xffffffffu, hmin, off));
-  if (lane == 0) b.Hmin[s & 1][gbase + (size_t)g * (L + 1) + (k - 1)] = hmin;
+  hh = __reduce_min_sync(0xffffffffu, hh);
+  if (lane == 0) b.Hmin[s & 1][gbase + (size_t)g * (L + 1) + (k - 1)] = __hiloint2double((int)hh, 0);
   if (__any_sync(0xffffffffu, anyfin) && lane == 0) {
     int2 *fr = &b.irange[s % 3][(size_t)group * (G + 1) + g];
     atomicMin(&fr->x, k - 1);

@@ -110,6 +110,7 @@ struct Batch {
   uint32_t *spart;     // [kParts][n_groups*cw] finite-cell counts of windowed
                        // layers, spread over kParts copies (dp_states_reduce)
   int n_opts;
+  int probe;           // best-first probe per staged chunk (HAPT_PROBE=0: off)
   double *H[2];        // [n_groups][G+1][L+1][cw]
   uint16_t *K[2];
   double *Hmin[2];     // [n_groups][G+1][L+1]: lower bound of H over the group's lanes
@@ -563,18 +564,50 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       int4 se = make_int4(0, 0, -1, 0);  // inert padding entry
       uint16_t sk = 0;
       bool keep = false;
+      double lb = kInf;  // tt + Hmin: no lane's value through this entry is lower
       if (t < T) {
         const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
         const int succ = oh + (x.w & 0xffff);
-        const double tt = __hiloint2double(x.y, x.x);
-        keep = __dadd_rn(tt, __ldg(Hm + succ)) < bmax;
+        lb = __dadd_rn(__hiloint2double(x.y, x.x), __ldg(Hm + succ));
+        keep = lb < bmax;
         const unsigned w2 =
             x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
         se = make_int4(x.x, x.y, (int)w2, succ * (256 * CPL));
         sk = (uint16_t)((unsigned)x.w >> 16);
       }
+      // Best-first probe: evaluate the kept entry with the smallest bound
+      // (position f) for every lane without recording it, which tightens the
+      // bound to bn = max over lanes of min(best, probe).  Every lane's final
+      // best is <= bn, so an entry after f with lb >= bn, or before f with
+      // lb > bn, is never the first minimum and is dropped; f itself stays
+      // and is relaxed in its own place, so the scan order is the reference's.
+      unsigned kept = __ballot_sync(0xffffffffu, keep);
+      if (b.probe && __popc(kept) > 2) {
+        const unsigned lh = keep ? (unsigned)__double2hiint(lb) : 0xffffffffu;
+        const unsigned ml = __reduce_min_sync(0xffffffffu, lh);
+        const int f = __ffs(__ballot_sync(0xffffffffu, keep && lh == ml)) - 1;
+        const int px = __shfl_sync(0xffffffffu, se.x, f), py = __shfl_sync(0xffffffffu, se.y, f);
+        const unsigned pz = __shfl_sync(0xffffffffu, (unsigned)se.z, f);
+        const unsigned pw = __shfl_sync(0xffffffffu, (unsigned)se.w, f);
+        const int pk = __shfl_sync(0xffffffffu, (int)sk, f);
+        double hp[CPL];
+        int kp[CPL];
+        load_h<CPL>(Hb + pw, hp);
+        if (anykk) load_k<CPL>(Kb + (pw >> 2), kp);
+        const double pt = __hiloint2double(py, px);
+        unsigned mh = 0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          double m = bv[c];
+          if (pz < cnt2[c] && (!anykk || kp[c] <= pk)) m = fmin(m, __dadd_rn(pt, hp[c]));
+          mh = max(mh, (unsigned)__double2hiint(m));
+        }
+        mh = __reduce_max_sync(0xffffffffu, mh);
+        const double bn = mh >= 0x7ff00000u ? kInf : __hiloint2double((int)mh, -1);
+        keep = keep && (lane == f || (lane < f ? lb <= bn : lb < bn));
+        kept = __ballot_sync(0xffffffffu, keep);
+      }
       // kept entries first, in order; the rest of the stage is inert
-      const unsigned kept = __ballot_sync(0xffffffffu, keep);
       const unsigned below = kept & ((1u << lane) - 1u);
       const int n = __popc(kept);
       if (keep) {
@@ -972,6 +1005,10 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.s_max = t->s_max;
   b.n_cand = n_cand;
   b.cpl = cpl_for(t, n_cand);
+  {
+    static const int probe = getenv("HAPT_PROBE") ? atoi(getenv("HAPT_PROBE")) : 1;
+    b.probe = probe;
+  }
   b.cw = 32 * b.cpl;
   b.n_groups = (n_cand + b.cw - 1) / b.cw;
   b.hg = (size_t)(t->G + 1) * (t->L + 1);

@@ -44,8 +44,7 @@ def main(names):
         out[name] = {"pool_candidates": len(pool), "reference_transitions": int(ref),
                      "executed_lane_transitions": int(w[0]),
                      "admissible_lane_transitions": int(w[1]),
-                     "improving_lane_transitions": int(w[2]),
-                     "warp_bound_skippable_lane_transitions": int(w[3])}
+                     "improving_lane_transitions": int(w[2])}
         print(name, out[name])
     out["source"] = "tools/work_counts.py (HAPT_COUNT_WORK build), one full-pool sweep each"
     dst = "gpurun_out" if os.path.isdir(os.path.join(REPO, "gpurun_out")) else "profiles"

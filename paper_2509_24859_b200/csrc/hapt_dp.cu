@@ -59,7 +59,14 @@ int cpl_for(const hapt_tables *t, int n_cand) {
   // a batch has more than ~240 candidates (7.5 groups of 32) on tables large
   // enough to fill the GPU -- below that the extra warps of CPL = 1 hide more
   // latency (D1: 16 candidates 2.55 -> 1.82 ms, 224 candidates 4.13 -> 3.79 ms)
-  const long warps2 = (long)t->L * t->G * ((n_cand + 63) / 64);
+  // With the lane-bound pruning the transition loop is short and the
+  // per-cell work (row metadata, staging, epilogue) dominates, so four
+  // candidates per lane pay off on large batches despite a few spilled
+  // registers (D1 1,786: 9.3 -> 7.2 ms; D2 7,019: 217 -> 144 ms; below
+  // ~1,000 candidates, or with too few warps per layer, CPL = 2 stays ahead)
+  const long cells = (long)t->L * t->G;
+  if (n_cand >= 1024 && cells * ((n_cand + 127) / 128) >= 80000) return 4;
+  const long warps2 = cells * ((n_cand + 63) / 64);
   return (warps2 >= 16384 && n_cand > 240) ? 2 : 1;
 }
 

@@ -766,7 +766,6 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   __shared__ unsigned s_cnt[2][CW];  // the block's first group and the next
   __shared__ unsigned s_done;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = b.G;
   const int total = b.goff[b.n_groups];
   const int idx0 = blockIdx.x * kWarps;
   if (idx0 >= total) return;  // whole block past the compact range

@@ -2,11 +2,13 @@
 goldens and the oracle."""
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
 import oracle as O
+from conftest import REPO
 from helpers import build, expected, expected_arrays, load_json, seeded
 
 pytestmark = pytest.mark.gpu
@@ -118,3 +120,29 @@ def test_batch_chunking_is_invisible():
     b = tables.sweeper.evaluate(pool, B)
     assert tables.sweeper.last_chunks == (len(pool) + 31) // 32
     assert np.array_equal(a.tstar, b.tstar) and np.array_equal(a.states, b.states)
+
+
+@pytest.mark.parametrize("env", [{"HAPT_CPL": "1"}, {"HAPT_CPL": "2"}, {"HAPT_CPL": "4"},
+                                 {"HAPT_PROBE": "0"}])
+def test_every_kernel_variant_equals_reference(env):
+    """Each candidates-per-lane variant of dp_relax, and the sweep without the
+    best-first probe, gives the reference's full-pool results (the library
+    reads these knobs once per process, hence the subprocess)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from helpers import build, load_json, expected_arrays\n"
+        "from paper_2509_24859_b200.planner import sweep_pool\n"
+        "for name in ('B', 'C', 'D1'):\n"
+        "    inst, arr = load_json(name), expected_arrays(name)\n"
+        "    store, costs, cluster, B, eps = build(inst)\n"
+        "    pool, tstar, best_s, states, winner = sweep_pool(store, costs, B)\n"
+        "    assert np.array_equal(tstar, arr['tstar']), name\n"
+        "    assert np.array_equal(best_s, arr['best_s']), name\n"
+        "    assert np.array_equal(states, arr['states']), name\n"
+        "print('ok')\n" % (REPO, os.path.dirname(os.path.abspath(__file__))))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       env={**os.environ, **env}, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]

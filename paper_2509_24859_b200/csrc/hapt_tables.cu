@@ -332,27 +332,37 @@ __global__ void k_fill_keys(unsigned long long *keys, size_t n) {
   if (i < n) keys[i] = kPadKey;
 }
 
+// One thread per CSR entry (the memory threshold is a 16-step binary search,
+// so a thread per row serialised up to L of them); the entry's row is found
+// by binary search over span_off.
 __global__ void k_span_meta(hapt_tables t, unsigned long long *keys) {
-  const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const int L = t.L, S = L + 2;
-  if (r >= (long)t.n_opts * S) return;
-  const int o = (int)(r / S);
-  const double cap = t.opt_cap[o];
-  const double *trow = t.t_tab + r * S, *mrow = t.mp_tab + r * S, *arow = t.ma_tab + r * S;
-  int kmin = kKSat;
-  for (int idx = t.span_off[r]; idx < t.span_off[r + 1]; ++idx) {
-    const int p = t.span_items[idx];
-    const double tt = trow[p];
-    hapt_span sp;
-    sp.tt = tt;
-    sp.prank = 0;
-    sp.i = (uint16_t)p;
-    const int km = mem_kmax(mrow[p], arow[p], cap);
-    sp.kmax = (uint16_t)km;
-    kmin = min(kmin, km);
-    t.spans[idx] = sp;
-    keys[idx] = isfinite(tt) ? fkey(tt) : kPadKey;
+  const long rows = (long)t.n_opts * S;
+  if (idx >= t.span_off[rows]) return;
+  long lo = 0, hi = rows;  // last row with span_off[row] <= idx
+  while (hi - lo > 1) {
+    const long mid = (lo + hi) >> 1;
+    if (t.span_off[mid] <= idx) lo = mid; else hi = mid;
   }
+  const long r = lo;
+  const int o = (int)(r / S);
+  const int p = t.span_items[idx];
+  const double tt = t.t_tab[r * S + p];
+  hapt_span sp;
+  sp.tt = tt;
+  sp.prank = 0;
+  sp.i = (uint16_t)p;
+  sp.kmax = (uint16_t)mem_kmax(t.mp_tab[r * S + p], t.ma_tab[r * S + p], t.opt_cap[o]);
+  t.spans[idx] = sp;
+  keys[idx] = isfinite(tt) ? fkey(tt) : kPadKey;
+}
+
+__global__ void k_row_kmin(hapt_tables t) {
+  const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (long)t.n_opts * (t.L + 2)) return;
+  int kmin = kKSat;
+  for (int idx = t.span_off[r]; idx < t.span_off[r + 1]; ++idx) kmin = min(kmin, (int)t.spans[idx].kmax);
   t.row_kmin[r] = (uint16_t)kmin;
 }
 
@@ -435,7 +445,8 @@ int finalize_impl(hapt_tables *tp, cudaStream_t st) {
   Layout y = layout(t.L, t.G, t.n_opts, t.n_meshes);
   const size_t rows = y.rows;
   k_fill_keys<<<grid_for(y.nnz_cap, 256), 256, 0, st>>>(s.keys_a, y.nnz_cap); ::hapt::note_launch();
-  k_span_meta<<<grid_for(rows, 128), 128, 0, st>>>(t, s.keys_a); ::hapt::note_launch();
+  k_span_meta<<<grid_for(y.nnz_cap, 128), 128, 0, st>>>(t, s.keys_a); ::hapt::note_launch();
+  k_row_kmin<<<grid_for(rows, 128), 128, 0, st>>>(t); ::hapt::note_launch();
   HAPT_LAUNCHED("k_span_meta");
   cub::DoubleBuffer<unsigned long long> db(s.keys_a, s.keys_b);
   size_t need = 0;

@@ -632,6 +632,24 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       __syncwarp();
     }
   }
+  // A warp with no finite best records nothing, and its successor entry is
+  // infinite for every lane: only Hmin = +inf is written, which makes the
+  // next layer drop every transition into it at staging (lb = +inf is never
+  // below a bound), so its H / K slots are never read and need no write.
+  // (ftop / N / bp keep their initial +inf / 0 / -1.)  A third of D1's cells
+  // end this way.
+  const size_t hm_idx = gbase + (size_t)g * (L + 1) + (k - 1);
+  {
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) any |= bw2[c] != ~0u;
+    if (!__any_sync(0xffffffffu, any)) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) fin[c] = 0;
+      if (lane == 0) b.Hmin[s & 1][hm_idx] = kInf;
+      return;
+    }
+  }
   // epilogue per candidate
   double hn[CPL];
   int kn[CPL];
@@ -677,19 +695,25 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       kn[c] = kcv + bkk;
     }
   }
-  const size_t o_idx = (gbase + (size_t)g * (L + 1) + (k - 1)) * CW + lane * CPL;
+  const size_t o_idx = hm_idx * CW + lane * CPL;
   bool anyfin = false;
   unsigned hh = 0xffffffffu;  // min over lanes of the high words; hi:0 bounds every H below
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
-    b.H[s & 1][o_idx + c] = hn[c];
-    b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
     anyfin |= hn[c] != kInf;
     hh = min(hh, (unsigned)__double2hiint(hn[c]));
   }
   hh = __reduce_min_sync(0xffffffffu, hh);
-  if (lane == 0) b.Hmin[s & 1][gbase + (size_t)g * (L + 1) + (k - 1)] = __hiloint2double((int)hh, 0);
-  if (__any_sync(0xffffffffu, anyfin) && lane == 0) {
+  if (lane == 0) b.Hmin[s & 1][hm_idx] = __hiloint2double((int)hh, 0);
+  const bool wfin = __any_sync(0xffffffffu, anyfin);
+  if (wfin) {  // otherwise Hmin = +inf already shields the slots (see above)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      b.H[s & 1][o_idx + c] = hn[c];
+      b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
+    }
+  }
+  if (wfin && lane == 0) {
     int2 *fr = &b.irange[s % 3][(size_t)group * (G + 1) + g];
     atomicMin(&fr->x, k - 1);
     atomicMax(&fr->y, k - 1);

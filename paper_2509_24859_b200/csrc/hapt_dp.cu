@@ -507,9 +507,15 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     bool needkk = false;
     if (lane < nch) {
       const int o = o0 + c0 + lane;
-      const int devs = b.opt_devs[o], g2 = g - devs;
+      const int row = o * (L + 2) + k;
+      // the row's own metadata does not depend on the successor range:
+      // loaded up front, beside the opt_devs -> irange -> row_pos chain
+      const int devs = __ldg(b.opt_devs + o);
+      const int cut = __ldg(b.cut_sr + (size_t)group * b.rows + row);
+      const int soff = __ldg(b.span_off + row);
+      const int kmin = __ldg(b.row_kmin + row);
+      const int g2 = g - devs;
       if (devs <= avail && g2 >= s - 1) {
-        const int row = o * (L + 2) + k;
         // admissible splits: i <= L-s+1 (later successors are provably
         // infinite), inside the range where state g2's successor entry is
         // finite for some candidate of the group, and before the group's
@@ -519,16 +525,16 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
         const int lo_i = max(k, fr.x), hi_i = min(imax, fr.y);
         if (lo_i <= hi_i) {
           const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
-          const int a = pos[lo_i - 1];
-          const int z = min((int)pos[hi_i], (int)b.cut_sr[(size_t)group * b.rows + row]);
-          beg = b.span_off[row] + a;
+          const int a = __ldg(pos + lo_i - 1);
+          const int z = min((int)__ldg(pos + hi_i), cut);
+          beg = soff + a;
           len = max(0, z - a);
         }
         hbase = g2 * (L + 1);
         // KK <= 3s at layer s: ceil(2c/t_max) <= 2 and N grows by <= 3 per
         // stage, so a row whose thresholds are all >= 3s cannot fail the
         // memory mask (_dp.pyx:83)
-        needkk = len > 0 && (int)b.row_kmin[row] < 3 * s;
+        needkk = len > 0 && kmin < 3 * s;
       }
     }
     int incl = len;

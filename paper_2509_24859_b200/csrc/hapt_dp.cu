@@ -73,6 +73,9 @@ int cpl_for(const hapt_tables *t, int n_cand) {
 #ifndef HAPT_U4
 #define HAPT_U4 2
 #endif
+#ifndef HAPT_PROBE_MIN
+#define HAPT_PROBE_MIN 2  // staged entries above which a chunk is probed
+#endif
 #ifndef HAPT_U2
 #define HAPT_U2 4  // 2, 4 or 8 (a 32-entry stage must be a multiple)
 #endif
@@ -595,7 +598,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       // lb > bn, is never the first minimum and is dropped; f itself stays
       // and is relaxed in its own place, so the scan order is the reference's.
       unsigned kept = __ballot_sync(0xffffffffu, keep);
-      if (b.probe && __popc(kept) > 2) {
+      if (b.probe && __popc(kept) > HAPT_PROBE_MIN) {
         const unsigned lh = keep ? (unsigned)__double2hiint(lb) : 0xffffffffu;
         const unsigned ml = __reduce_min_sync(0xffffffffu, lh);
         const int f = __ffs(__ballot_sync(0xffffffffu, keep && lh == ml)) - 1;

@@ -111,7 +111,8 @@ struct Batch {
   uint32_t *clist;     // [n_groups][ccap] (g << 16 | k) of the cells inside the
                        // current layer's windows, group-local compact order
   size_t ccap;         // L*G >= cells of any layer
-  int32_t *gtot;       // [n_groups] window cells per group
+  int32_t *gtot;       // [n_groups] window cells per group, reserved by
+                       // dp_window's warps (zero between windowed layers)
   int32_t *goff;       // [n_groups+1] exclusive prefix of gtot: the compact cell
                        // index space dp_relax_compact walks
   unsigned *ticket;    // dp_window's last-block counter (self-resetting)
@@ -186,6 +187,7 @@ __global__ void dp_prep(Batch b) {
   const int cw = b.cw;
   if (threadIdx.x == 0) s_gmax = 0;
   if (group == 0 && threadIdx.x == 0) *b.ticket = 0u;
+  if (threadIdx.x == 0) b.gtot[group] = 0;
   __syncthreads();
   double *H = b.H[0] + (size_t)group * b.hg * cw;
   uint16_t *K = b.K[0] + (size_t)group * b.hg * cw;
@@ -284,107 +286,102 @@ __global__ void dp_prep(Batch b) {
 // k in [lo - maxlen_o + 1, min(hi, L-s+1)].  Cells outside the hull are
 // provably infinite and are never read by layer s+1 (its read range comes
 // from cells that were finite), so dp_relax skips them without writing.
-// Block-wide exclusive scan of one int per thread (blockDim.x a multiple of
-// 32, at most kWinThreads).
-constexpr int kWinThreads = 1024;
-__device__ __forceinline__ int block_excl_scan(int v, int &total) {
-  __shared__ int wsum[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += y;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  int before = 0;
-  total = 0;
-#pragma unroll
-  for (int w = 0; w < 32; ++w) {
-    const int x = w < (int)(blockDim.x >> 5) ? wsum[w] : 0;
-    before += w < warp ? x : 0;
-    total += x;
-  }
-  __syncthreads();  // wsum reusable
-  return before + incl - v;
-}
-
 // Per layer and group: the window [klo, khi] of every state g (cells outside
 // are provably infinite: no option can reach a finite successor from them),
-// the compact enumeration of the cells inside (clist / gtot, then goff by the
-// last block), and the reset of the irange buffer layer s+1 writes (last read
-// by layer s-1).
-__global__ void __launch_bounds__(kWinThreads) dp_window(Batch b, int s) {
+// the compact enumeration of the cells inside, and the reset of the irange
+// buffer layer s+1 writes (last read by layer s-1).  One thread per state,
+// kWinBlock states per block and blockIdx.y = group, so the per-state
+// dependent-load chains of a layer run on many SMs at once; each warp
+// reserves its states' cells in the group's list with one atomic (the order
+// of states in the list does not matter: cells are independent), and the
+// last block turns the group totals into goff.
+constexpr int kWinBlock = 64;
+__global__ void __launch_bounds__(kWinBlock) dp_window(Batch b, int s) {
   pdl_wait();
   pdl_trigger();
-  const int group = blockIdx.x;
+  const int group = blockIdx.y;
   const int L = b.L, G = b.G, imax = L - s + 1;
-  int carry = 0;
-  for (int g0 = 0; g0 <= G; g0 += blockDim.x) {
-    const int g = g0 + threadIdx.x;
-    int klo = 0x7fff, khi = 0;
-    if (g <= G && g >= s) {
-      const int r = b.g_mesh[g], avail = b.g_avail[g];
-      const int oa = b.opt_off[r], ob = b.opt_off[r + 1];
-      // four options at a time with independent loads (the per-thread chain
-      // of dependent loads is this kernel's whole cost)
-      for (int o0 = oa; o0 < ob; o0 += 4) {
-        int2 fr[4];
-        int ml[4];
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kWinBlock + threadIdx.x;
+  int klo = 0x7fff, khi = 0;
+  if (g <= G && g >= s) {
+    const int r = b.g_mesh[g], avail = b.g_avail[g];
+    const int oa = b.opt_off[r], ob = b.opt_off[r + 1];
+    // four options at a time with independent loads (the per-thread chain
+    // of dependent loads is this kernel's whole cost)
+    for (int o0 = oa; o0 < ob; o0 += 4) {
+      int2 fr[4];
+      int ml[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int o = o0 + u;
-          fr[u] = make_int2(1, 0);
-          ml[u] = 0;
-          if (o < ob) {
-            const int devs = b.opt_devs[o], g2 = g - devs;
-            if (devs <= avail && g2 >= s - 1) {
-              fr[u] = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
-              ml[u] = b.maxlen[(size_t)group * b.n_opts + o];
-            }
+      for (int u = 0; u < 4; ++u) {
+        const int o = o0 + u;
+        fr[u] = make_int2(1, 0);
+        ml[u] = 0;
+        if (o < ob) {
+          const int devs = b.opt_devs[o], g2 = g - devs;
+          if (devs <= avail && g2 >= s - 1) {
+            fr[u] = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
+            ml[u] = b.maxlen[(size_t)group * b.n_opts + o];
           }
         }
+      }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int hi = min(imax, fr[u].y);
-          if (fr[u].x > hi || ml[u] == 0) continue;
-          klo = min(klo, max(1, fr[u].x - ml[u] + 1));
-          khi = max(khi, hi);
-        }
+      for (int u = 0; u < 4; ++u) {
+        const int hi = min(imax, fr[u].y);
+        if (fr[u].x > hi || ml[u] == 0) continue;
+        klo = min(klo, max(1, fr[u].x - ml[u] + 1));
+        khi = max(khi, hi);
       }
     }
-    const int n = khi >= klo ? khi - klo + 1 : 0;
-    int tile;
-    const int off = carry + block_excl_scan(n, tile);
-    if (g <= G) {
-      uint32_t *cl = b.clist + (size_t)group * b.ccap + off;
-      for (int t = 0; t < n; ++t) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t);
-      b.irange[(s + 1) % 3][(size_t)group * (G + 1) + g] = make_int2(0x7fffffff, -1);
-    }
-    carry += tile;
+  }
+  const int n = khi >= klo ? khi - klo + 1 : 0;
+  // warp-exclusive prefix and one reservation per warp
+  int incl = n;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+  int base = 0;
+  int32_t *cnt = b.gtot + group;
+  if (lane == 31 && wtot > 0) base = atomicAdd(cnt, wtot);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  if (g <= G) {
+    uint32_t *cl = b.clist + (size_t)group * b.ccap + base + (incl - n);
+    for (int t = 0; t < n; ++t) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t);
+    b.irange[(s + 1) % 3][(size_t)group * (G + 1) + g] = make_int2(0x7fffffff, -1);
   }
   __shared__ bool last;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    b.gtot[group] = carry;
     __threadfence();
-    last = atomicAdd(b.ticket, 1u) == gridDim.x - 1;
+    last = atomicAdd(b.ticket, 1u) == gridDim.x * gridDim.y - 1;
   }
   __syncthreads();
   if (!last) return;
-  // last block: exclusive prefix of the group totals
+  // last block (every reservation is in): exclusive prefix of the group
+  // totals, which are then zeroed for the next windowed layer
   __threadfence();
-  int base = 0;
-  for (int j0 = 0; j0 < b.n_groups; j0 += blockDim.x) {
-    const int j = j0 + threadIdx.x;
-    const int v = j < b.n_groups ? __ldcg(b.gtot + j) : 0;
-    int tile;
-    const int off = base + block_excl_scan(v, tile);
-    if (j < b.n_groups) b.goff[j] = off;
-    base += tile;
+  int32_t *tot = b.gtot;
+  int run = 0;
+  for (int j0 = 0; j0 < b.n_groups; j0 += 32) {
+    const int j = j0 + lane;
+    const int v = (threadIdx.x < 32 && j < b.n_groups) ? __ldcg(tot + j) : 0;
+    int in2 = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, in2, off);
+      if (lane >= off) in2 += y;
+    }
+    if (threadIdx.x < 32 && j < b.n_groups) {
+      b.goff[j] = run + in2 - v;
+      tot[j] = 0;
+    }
+    run += __shfl_sync(0xffffffffu, in2, 31);
   }
   if (threadIdx.x == 0) {
-    b.goff[b.n_groups] = base;
+    b.goff[b.n_groups] = run;
     *b.ticket = 0u;
   }
 }
@@ -1101,9 +1098,8 @@ int run_sweep(const Batch &b, cudaStream_t st) {
                                                           : 32768;
     const int use_window = cells * b.n_groups >= win_min;
     if (use_window) {
-      // one thread per state g (G+1 <= 1024 in one pass)
-      const int wt = min(kWinThreads, (b.G + 1 + 31) / 32 * 32);
-      HAPT_CUDA(launch_pdl(dp_window, b.n_groups, wt, st, pdl, b, s));
+      const dim3 wgrid((b.G + 1 + kWinBlock - 1) / kWinBlock, b.n_groups);
+      HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinBlock, st, pdl, b, s));
       const unsigned cgrid = grid_for((size_t)cells * b.n_groups, kWarps);
       const dim3 blk(kWarps * 32);
       if (b.cpl == 1)

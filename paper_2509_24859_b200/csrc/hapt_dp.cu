@@ -65,7 +65,8 @@ int cpl_for(const hapt_tables *t, int n_cand) {
   // registers (D1 1,786: 9.3 -> 7.2 ms; D2 7,019: 217 -> 144 ms; below
   // ~1,000 candidates, or with too few warps per layer, CPL = 2 stays ahead)
   const long cells = (long)t->L * t->G;
-  if (n_cand >= 1024 && cells * ((n_cand + 127) / 128) >= 80000) return 4;
+  const long warps4 = cells * ((n_cand + 127) / 128);
+  if ((n_cand >= 1024 && warps4 >= 80000) || (n_cand >= 640 && warps4 >= 120000)) return 4;
   const long warps2 = cells * ((n_cand + 63) / 64);
   return (warps2 >= 16384 && n_cand > 240) ? 2 : 1;
 }

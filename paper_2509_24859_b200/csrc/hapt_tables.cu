@@ -397,21 +397,37 @@ __global__ void k_prank(hapt_tables t) {
 
 // Row suffix-min pool ranks and the per-row position table row_pos[row][i]
 // = #entries with span end <= i (entries are in ascending span end).
+// One warp per row (a thread per row walked up to L entries twice, one
+// dependent load at a time): suffix minimum of the pool ranks from the row's
+// end in 32-entry chunks, then row_pos[i] = #entries with span end <= i by a
+// binary search per i (entries are in ascending span end).
 __global__ void k_srank(hapt_tables t) {
-  const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long r = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   const int S = t.L + 2;
-  if (r >= (long)t.n_opts * S) return;
-  int m = 0x7fffffff;
+  if (r >= (long)t.n_opts * S) return;  // warp-uniform
   const int beg = t.span_off[r], end = t.span_off[r + 1];
-  for (int idx = end - 1; idx >= beg; --idx) {
-    m = min(m, t.spans[idx].prank);
-    t.span_srank[idx] = m;
+  int carry = 0x7fffffff;
+  for (int c1 = end; c1 > beg; c1 -= 32) {  // chunk [c1-32, c1)
+    const int idx = c1 - 32 + lane;
+    int m = idx >= beg ? t.spans[idx].prank : 0x7fffffff;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_down_sync(0xffffffffu, m, off);
+      if (lane + off < 32) m = min(m, y);
+    }
+    m = min(m, carry);
+    if (idx >= beg) t.span_srank[idx] = m;
+    carry = __shfl_sync(0xffffffffu, m, 0);
   }
   uint16_t *pos = t.row_pos + r * S;
-  int idx = beg;
-  for (int i = 0; i < S; ++i) {
-    while (idx < end && t.spans[idx].i <= i) ++idx;
-    pos[i] = (uint16_t)(idx - beg);
+  for (int i = lane; i < S; i += 32) {
+    int lo = beg, hi = end;  // first entry with span end > i
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)t.spans[mid].i <= i) lo = mid + 1; else hi = mid;
+    }
+    pos[i] = (uint16_t)(lo - beg);
   }
 }
 
@@ -468,7 +484,7 @@ int finalize_impl(hapt_tables *tp, cudaStream_t st) {
   HAPT_CUDA(cub::DeviceSelect::Unique(s.cub_temp, need, sorted, uniq, num_unique, (int)y.nnz_cap, st));
   k_pool_decode<<<grid_for(y.pool_cap, 256), 256, 0, st>>>(t, uniq, num_unique); ::hapt::note_launch();
   k_prank<<<grid_for(y.nnz_cap, 256), 256, 0, st>>>(t); ::hapt::note_launch();
-  k_srank<<<grid_for(rows, 128), 128, 0, st>>>(t); ::hapt::note_launch();
+  k_srank<<<grid_for(rows * 32, 256), 256, 0, st>>>(t); ::hapt::note_launch();
   k_gcrow<<<grid_for(t.G + 1, 128), 128, 0, st>>>(t); ::hapt::note_launch();
   HAPT_LAUNCHED("finalize");
   return HAPT_OK;

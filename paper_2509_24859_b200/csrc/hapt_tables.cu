@@ -197,12 +197,15 @@ __global__ void k1_canon(int L, int dedup, const int32_t *lcp, int32_t *canon) {
   }
   int c = q;
   if (dedup) {
+    // first a < q with lcp >= len, eight independent loads per step
     const int len = p - q + 1;
-    for (int a = 1; a < q; ++a) {
-      if (lcp[a * (L + 2) + q] >= len) {
-        c = a;
-        break;
-      }
+    for (int a0 = 1; a0 < q && c == q; a0 += 8) {
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = a0 + u < q ? lcp[(a0 + u) * (L + 2) + q] : -1;
+#pragma unroll
+      for (int u = 7; u >= 0; --u)
+        if (v[u] >= len) c = a0 + u;
     }
   }
   canon[x] = c;

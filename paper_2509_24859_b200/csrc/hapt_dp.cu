@@ -794,56 +794,53 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   constexpr int CW = 32 * CPL;
   __shared__ int4 stage_e[kWarps][32];
   __shared__ uint16_t stage_k[kWarps][32];
-  __shared__ unsigned s_cnt[2][CW];  // the block's first group and the next
-  __shared__ unsigned s_done;
+  __shared__ unsigned s_cnt[2][CW];  // the unit's first group and the next
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int total = b.goff[b.n_groups];
-  const int idx0 = blockIdx.x * kWarps;
-  if (idx0 >= total) return;  // whole block past the compact range
-  for (int x = threadIdx.x; x < 2 * CW; x += blockDim.x) (&s_cnt[0][0])[x] = 0u;
-  if (threadIdx.x == 0) s_done = 0u;
-  __syncthreads();
-  const int group0 = find_group(b.goff, b.n_groups, idx0, lane);
-  const int idx = idx0 + warp;
-  if (idx < total) {
-    const int group = find_group(b.goff, b.n_groups, idx, lane);
-    const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
-    const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
-    int fin[CPL];
-    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
-    const int slot = group - group0;  // a block spans 8 cells: almost always 0 or 1
+  // units of kWarps consecutive cells, strided over the grid (the grid is
+  // the upper bound of the list, or fewer blocks that loop)
+  for (int idx0 = blockIdx.x * kWarps; idx0 < total; idx0 += gridDim.x * kWarps) {
+    for (int x = threadIdx.x; x < 2 * CW; x += blockDim.x) (&s_cnt[0][0])[x] = 0u;
+    __syncthreads();
+    const int group0 = find_group(b.goff, b.n_groups, idx0, lane);
+    const int idx = idx0 + warp;
+    if (idx < total) {
+      const int group = find_group(b.goff, b.n_groups, idx, lane);
+      const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
+      const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
+      int fin[CPL];
+      relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
+      const int slot = group - group0;  // a unit spans 8 cells: almost always 0 or 1
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      if (!fin[c]) continue;
-      if (slot < 2)
-        atomicAdd(&s_cnt[slot][lane * CPL + c], 1u);
-      else  // third group inside one block (tiny groups): straight to a copy
-        atomicAdd(b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW +
-                      (size_t)group * CW + lane * CPL + c, 1u);
-    }
-  }
-  __threadfence_block();
-  unsigned done = 0;
-  if (lane == 0) done = atomicAdd(&s_done, 1u);
-  done = __shfl_sync(0xffffffffu, done, 0);
-  if (done != kWarps - 1) return;
-  // last warp of the block: flush both slots
-  __threadfence_block();
-  uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
-  for (int slot = 0; slot < 2 && group0 + slot < b.n_groups; ++slot) {
-    uint32_t *dst = part + (size_t)(group0 + slot) * CW + lane * CPL;
-    const volatile unsigned *src = &s_cnt[slot][lane * CPL];
-    if constexpr (CPL == 1) {
-      if (src[0]) atomicAdd(dst, src[0]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < CPL; c += 2) {
-        const unsigned lo = src[c], hi = src[c + 1];
-        if (lo | hi)
-          atomicAdd(reinterpret_cast<unsigned long long *>(dst + c),
-                    (unsigned long long)lo | ((unsigned long long)hi << 32));
+      for (int c = 0; c < CPL; ++c) {
+        if (!fin[c]) continue;
+        if (slot < 2)
+          atomicAdd(&s_cnt[slot][lane * CPL + c], 1u);
+        else  // third group inside one unit (tiny groups): straight to a copy
+          atomicAdd(b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW +
+                        (size_t)group * CW + lane * CPL + c, 1u);
       }
     }
+    __syncthreads();
+    if (warp == 0) {  // flush both slots
+      uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
+      for (int slot = 0; slot < 2 && group0 + slot < b.n_groups; ++slot) {
+        uint32_t *dst = part + (size_t)(group0 + slot) * CW + lane * CPL;
+        const unsigned *src = &s_cnt[slot][lane * CPL];
+        if constexpr (CPL == 1) {
+          if (src[0]) atomicAdd(dst, src[0]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < CPL; c += 2) {
+            const unsigned lo = src[c], hi = src[c + 1];
+            if (lo | hi)
+              atomicAdd(reinterpret_cast<unsigned long long *>(dst + c),
+                        (unsigned long long)lo | ((unsigned long long)hi << 32));
+          }
+        }
+      }
+    }
+    __syncthreads();  // s_cnt is reused by the next unit
   }
 }
 
@@ -1101,7 +1098,18 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     if (use_window) {
       const dim3 wgrid((b.G + 1 + kWinBlock - 1) / kWinBlock, b.n_groups);
       HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinBlock, st, pdl, b, s));
-      const unsigned cgrid = grid_for((size_t)cells * b.n_groups, kWarps);
+      // the compact list's length is only known on the device: the grid is
+      // its upper bound, capped at 32 blocks per SM that loop over the units
+      // (measured: launching the bound's mostly empty blocks cost ~4 % of a
+      // D1 pool sweep; 24-40 blocks per SM are within noise)
+      static const unsigned gcap = [] {
+        if (const char *e = getenv("HAPT_RELAX_GRID")) return (unsigned)atoi(e);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return 32u * (unsigned)sms;
+      }();
+      const unsigned cgrid = min(gcap, grid_for((size_t)cells * b.n_groups, kWarps));
       const dim3 blk(kWarps * 32);
       if (b.cpl == 1)
         HAPT_CUDA(launch_pdl(dp_relax_compact<1>, cgrid, blk, st, pdl, b, s));

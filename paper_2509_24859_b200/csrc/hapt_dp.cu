@@ -36,7 +36,10 @@ namespace {
 #ifdef HAPT_COUNT_WORK
 __device__ unsigned long long g_work[4];  // executed / admissible / improving
 #endif
-constexpr int kWarps = 8;  // warps (cells) per block
+#ifndef HAPT_KWARPS
+#define HAPT_KWARPS 8
+#endif
+constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
 #ifndef HAPT_RELAX_MINB
 #define HAPT_RELAX_MINB 4  // resident blocks/SM (64 registers, no spills: ptxas -v)

@@ -41,6 +41,9 @@ __device__ unsigned long long g_work[4];  // executed / admissible / improving
 #endif
 constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
+#ifndef HAPT_RELAX_WARPLOOP
+#define HAPT_RELAX_WARPLOOP 1  // 0: units of kWarps cells with block barriers (v14)
+#endif
 #ifndef HAPT_RELAX_MINB
 #define HAPT_RELAX_MINB 4  // resident blocks/SM (64 registers, no spills: ptxas -v)
 #endif
@@ -797,9 +800,47 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   constexpr int CW = 32 * CPL;
   __shared__ int4 stage_e[kWarps][32];
   __shared__ uint16_t stage_k[kWarps][32];
-  __shared__ unsigned s_cnt[2][CW];  // the unit's first group and the next
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int total = b.goff[b.n_groups];
+#if HAPT_RELAX_WARPLOOP
+  // Barrier-free variant: every warp strides over the list on its own and
+  // keeps its finite-cell counts in registers while its cells stay in one
+  // group, flushing them to a counter copy when the group changes.
+  uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
+  int cur = -1;
+  unsigned cnt[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) cnt[c] = 0u;
+  auto flush = [&](int grp) {
+    uint32_t *dst = part + (size_t)grp * CW + lane * CPL;
+    if constexpr (CPL == 1) {
+      if (cnt[0]) atomicAdd(dst, cnt[0]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; c += 2)
+        if (cnt[c] | cnt[c + 1])
+          atomicAdd(reinterpret_cast<unsigned long long *>(dst + c),
+                    (unsigned long long)cnt[c] | ((unsigned long long)cnt[c + 1] << 32));
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) cnt[c] = 0u;
+  };
+  for (int idx = blockIdx.x * kWarps + warp; idx < total; idx += gridDim.x * kWarps) {
+    const int group = find_group(b.goff, b.n_groups, idx, lane);
+    if (group != cur) {
+      if (cur >= 0) flush(cur);
+      cur = group;
+    }
+    const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
+    const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
+    int fin[CPL];
+    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) cnt[c] += fin[c] ? 1u : 0u;
+  }
+  if (cur >= 0) flush(cur);
+#else
+  __shared__ unsigned s_cnt[2][CW];  // the unit's first group and the next
   // units of kWarps consecutive cells, strided over the grid (the grid is
   // the upper bound of the list, or fewer blocks that loop)
   for (int idx0 = blockIdx.x * kWarps; idx0 < total; idx0 += gridDim.x * kWarps) {
@@ -845,6 +886,7 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     }
     __syncthreads();  // s_cnt is reused by the next unit
   }
+#endif
 }
 
 // states[cand] += sum of the kParts partial counters (padding lanes dropped)

@@ -37,7 +37,7 @@ namespace {
 __device__ unsigned long long g_work[4];  // executed / admissible / improving
 #endif
 #ifndef HAPT_KWARPS
-#define HAPT_KWARPS 8
+#define HAPT_KWARPS 4
 #endif
 constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
@@ -45,7 +45,7 @@ constexpr int kParts = 32;  // copies of the per-candidate state counters
 #define HAPT_RELAX_WARPLOOP 1  // 0: units of kWarps cells with block barriers (v14)
 #endif
 #ifndef HAPT_RELAX_MINB
-#define HAPT_RELAX_MINB 4  // resident blocks/SM (64 registers, no spills: ptxas -v)
+#define HAPT_RELAX_MINB 8  // resident blocks/SM (64 registers at 4 warps per block)
 #endif
 
 // Candidates per lane.  A group of 32*CPL candidates shares one warp per DP
@@ -787,11 +787,11 @@ __device__ __forceinline__ int find_group(const int32_t *__restrict__ goff, int 
 
 // Windowed layers: only the cells inside dp_window's windows, enumerated
 // compactly (group-major, then g, then k), one warp per cell over an
-// upper-bound grid (surplus blocks exit at once) -- no warp is spent on a
-// provably infinite cell.  Finite-cell counts are combined per block in
-// shared memory and flushed by whichever warp finishes last, so no warp waits
-// at a barrier for a slower one; the flush goes to one of kParts counter
-// copies (dp_states_reduce sums them) to avoid a same-address atomic hot spot.
+// grid capped at 256 warps per SM that stride over the list -- no warp is
+// spent on a provably infinite cell.  Finite-cell counts go to one of kParts
+// counter copies (dp_states_reduce sums them) to avoid a same-address atomic
+// hot spot; by default (HAPT_RELAX_WARPLOOP) each warp keeps them in
+// registers and no warp waits at a block barrier for a slower one.
 template <int CPL>
 __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     dp_relax_compact(Batch b, int s) {
@@ -1144,15 +1144,15 @@ int run_sweep(const Batch &b, cudaStream_t st) {
       const dim3 wgrid((b.G + 1 + kWinBlock - 1) / kWinBlock, b.n_groups);
       HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinBlock, st, pdl, b, s));
       // the compact list's length is only known on the device: the grid is
-      // its upper bound, capped at 32 blocks per SM that loop over the units
+      // its upper bound, capped at 256 warps per SM that loop over the cells
       // (measured: launching the bound's mostly empty blocks cost ~4 % of a
-      // D1 pool sweep; 24-40 blocks per SM are within noise)
+      // D1 pool sweep; 128 warps per SM: +2.5 %, 512: +2.6 % at kWarps 8)
       static const unsigned gcap = [] {
         if (const char *e = getenv("HAPT_RELAX_GRID")) return (unsigned)atoi(e);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        return 32u * (unsigned)sms;
+        return (256u / kWarps) * (unsigned)sms;
       }();
       const unsigned cgrid = min(gcap, grid_for((size_t)cells * b.n_groups, kWarps));
       const dim3 blk(kWarps * 32);

@@ -148,7 +148,8 @@ typedef struct {
   double *pool;         /* [pool_cap] sorted unique feasible t (t_max candidates) */
   int64_t *counters;    /* [16]: 0 nnz, 1 pool_len, 2..7 StoreStats
                            (candidates, canonical, canonical_feasible, aliased,
-                           pruned_oom, pruned_imbalance)                     */
+                           pruned_oom, pruned_imbalance), 10 = 1 if the
+                           remaining-device encoding is unsupported (below) */
   void *scratch;        /* internal                                          */
   size_t scratch_bytes;
 } hapt_tables;
@@ -163,7 +164,14 @@ int hapt_tables_init(hapt_tables *t, void *buf, size_t buf_bytes, int32_t L,
 int hapt_tables_build(hapt_tables *t, const hapt_model_desc *desc, void *stream);
 /* Given t_tab/mp_tab/ma_tab/opt_cap/opt_mesh/opt_devs/opt_off/cb_same/cb_next/
  * g_mesh/g_avail/span_off/span_items already in place, derive spans, span_ik,
- * g_crow, pool and counters[0..1]. s_max is taken from t->s_max. */
+ * g_crow, pool and counters[0..1]. s_max is taken from t->s_max.
+ * Encoding requirement (checked on the device, counters[10] = 1 if violated;
+ * the drop-in dp_sweep raises ValueError then): every option uses >= 1
+ * device, g_mesh[1..G] names a mesh, and the boundary row a transition into
+ * state g2 reads (cb_same[r] if g_mesh[g2] == r else cb_next[r], r the
+ * caller's mesh, _dp.pyx:64-77) is the same for every caller of g2.
+ * DpTables' encoding (planner.py:213-226, meshes consumed in order) always
+ * satisfies it; the reference's Cython kernel accepts any encoding. */
 int hapt_tables_finalize(hapt_tables *t, void *stream);
 
 /* ------------------------------------------------------------------------ */

@@ -298,3 +298,37 @@ int32_t oracle_adaptive_counts(int32_t S, const double *stage_t, const double *c
   }
   return 0;
 }
+
+/* Config E batch (checker for the 10^5+-plan parity test): per plan p of
+ * dense [P][8] inputs, adaptive counts with epsilon and t_max = max stage
+ * time (scheduling.py:89-124), then the explicit-DAG makespan of
+ * oracle_simulate (simulation.py:73-228).  status[p] = 0, or the boundary of
+ * a CommTooLargeError.  Plans are independent, so `lo..hi` lets the caller
+ * split the batch over host threads. */
+void oracle_config_e_batch(int64_t lo, int64_t hi, int32_t B, const int32_t *S,
+                           const double *t_fwd, const double *t_bwd, const double *comm,
+                           double epsilon, int32_t *counts, int32_t *status, double *makespan) {
+  long cap = 0;
+  double *start = NULL, *end = NULL;
+  for (int64_t p = lo; p < hi; ++p) {
+    const int s = S[p];
+    double st[8];
+    for (int i = 0; i < s; ++i) st[i] = t_fwd[p * 8 + i] + t_bwd[p * 8 + i];
+    status[p] = oracle_adaptive_counts(s, st, comm + p * 8, epsilon, NAN, counts + p * 8);
+    makespan[p] = NAN;
+    if (status[p]) continue;
+    const long n = (long)B * (4L * s - 2) + 1;
+    if (n > cap) {
+      free(start);
+      free(end);
+      start = malloc(n * sizeof(double));
+      end = malloc(n * sizeof(double));
+      cap = n;
+    }
+    if (oracle_simulate(s, B, t_fwd + p * 8, t_bwd + p * 8, comm + p * 8, counts + p * 8, start,
+                        end, makespan + p) != n)
+      status[p] = -1; /* dependency cycle */
+  }
+  free(start);
+  free(end);
+}

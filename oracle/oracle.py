@@ -50,6 +50,8 @@ def lib():
         _lib.oracle_simulate.restype = ctypes.c_long
         _lib.oracle_adaptive_counts.argtypes = [i32, P, P, d, d, P]
         _lib.oracle_adaptive_counts.restype = i32
+        _lib.oracle_config_e_batch.argtypes = [i64, i64, i32, P, P, P, P, d, P, P, P]
+        _lib.oracle_config_e_batch.restype = None
     return _lib
 
 
@@ -499,6 +501,31 @@ def schedule_report(t_fwd, t_bwd, comm, counts, B: int, mem_act=None):
         rate = (sum((x - mx) * (y - my) for x, y in zip(xs, ys))
                 / sum((x - mx) ** 2 for x in xs))
     return mk, stages, links, rate
+
+
+def config_e_batch(t_fwd, t_bwd, comm, S, B: int = 128, epsilon: float = 0.05,
+                   threads: int | None = None):
+    """Adaptive counts + explicit-DAG makespan of every plan of dense [P, 8]
+    inputs (oracle_config_e_batch), split over host threads.  Returns
+    (counts [P, 8] int32, status [P] int32, makespan [P] float64)."""
+    f = np.ascontiguousarray(t_fwd, dtype=np.float64)
+    b = np.ascontiguousarray(t_bwd, dtype=np.float64)
+    c = np.ascontiguousarray(comm, dtype=np.float64)
+    s = np.ascontiguousarray(S, dtype=np.int32)
+    P = len(s)
+    counts = np.zeros((P, 8), dtype=np.int32)
+    status = np.zeros(P, dtype=np.int32)
+    mk = np.full(P, np.nan)
+    threads = threads or os.cpu_count() or 1
+    step = (P + threads - 1) // threads
+
+    def run(lo):
+        lib().oracle_config_e_batch(lo, min(P, lo + step), B, _p(s), _p(f), _p(b), _p(c),
+                                    float(epsilon), _p(counts), _p(status), _p(mk))
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, range(0, P, step)))
+    return counts, status, mk
 
 
 def config_e_plans(n_plans: int, seed: int = 24859, B: int = 128):

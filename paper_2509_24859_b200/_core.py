@@ -4,15 +4,25 @@
 reference operator (_dp.pyx:14-28; dp_py.py:27-43): numpy inputs in the
 DpTables layout, numpy outputs F, N (float64) and bp_i, bp_o (int32) of shape
 [s_max+1, L+2, G+1].  The sweep runs on the GPU (hapt_tables_finalize +
-hapt_dp_sweep_batch with full outputs); a reference caller such as
+hapt_dp_sweep with full outputs); a reference caller such as
 planner.dp_search or benchmarks/bench_dp.py can be pointed at it unchanged
 by rebinding the reference module attribute `planner.dp_sweep` to this
-function (INTEGRATION.md shows the one-line binding).
+function (INTEGRATION.md shows the one-line binding; tests/test_gpu_dropin.py
+runs the reference's own search() through it).
+
+Encodings: any (g_mesh, g_avail) the DP's successor-table hoisting can
+represent is accepted -- every option uses >= 1 device and the boundary row
+of a transition is a function of its successor state (include/hapt_b200.h,
+hapt_tables_finalize).  DpTables' encoding always qualifies; others raise
+ValueError instead of returning different tables.
 
 There is no CPU fallback: without the CUDA library this module raises.
 """
 
 from __future__ import annotations
+
+import threading
+from collections import OrderedDict
 
 import numpy as np
 
@@ -20,42 +30,49 @@ from .engine import DeviceTables, Sweeper
 
 BACKEND = "cuda"
 
-_cache: dict = {}
+# The reference calls dp_sweep from ThreadPoolExecutor workers
+# (planner.py:529-531), and the Cython kernel is reentrant.  Here one lock
+# covers the whole call -- table lookup/upload, the ~2 launches per layer on
+# the shared per-stream workspace, and the device-to-host copies -- so
+# concurrent calls are serialised instead of interleaving their kernels on
+# one scratch buffer.  Table sets are cached per call key (several DpTables
+# may be in use at once), least recently used first out.
+_lock = threading.Lock()
+_cache: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_MAX = 4
 
 
-def _check_encoding(g_mesh: np.ndarray, g_avail: np.ndarray, opt_off: np.ndarray) -> None:
-    """The device kernel reads the successor state's boundary row from g alone,
-    which holds for the DpTables encoding (planner.py:213-226): meshes consumed
-    in order, g_avail counting up inside each mesh."""
-    G = len(g_mesh) - 1
-    for g in range(1, G + 1):
-        m = int(g_mesh[g])
-        if g > 1 and int(g_mesh[g - 1]) != m:
-            if int(g_mesh[g - 1]) != m + 1 or int(g_avail[g]) != 1:
-                raise ValueError("dp_sweep: unsupported remaining-device encoding")
-        elif g > 1 and int(g_avail[g]) != int(g_avail[g - 1]) + 1:
-            raise ValueError("dp_sweep: unsupported remaining-device encoding")
-        if not 0 <= m < len(opt_off) - 1:
-            raise ValueError("dp_sweep: g_mesh out of range")
-    if G >= 1 and int(g_avail[1]) != 1:
-        raise ValueError("dp_sweep: unsupported remaining-device encoding")
-
-
-def _device_tables(args: dict, s_max: int) -> DeviceTables:
-    """Tables are cached on the identity of the caller's arrays (DpTables keeps
-    them alive for a whole search), so repeated sweeps skip the upload."""
+def _entry(args: dict, s_max: int):
+    """(DeviceTables, Sweeper) for these arrays.  Tables are cached on the
+    identity of the caller's arrays (DpTables keeps them alive for a whole
+    search), so repeated sweeps skip the upload; the entry also holds the
+    arrays, so an id cannot be recycled while its entry lives."""
     key = tuple(id(args[k]) for k in sorted(args)) + (s_max,)
     hit = _cache.get(key)
     if hit is not None and all(hit[1][k] is args[k] for k in args):
-        return hit[0]
+        _cache.move_to_end(key)
+        return hit[0], hit[2]
     L = args["t_tab"].shape[1] - 2
     G = args["g_mesh"].shape[0] - 1
     n_opts = args["t_tab"].shape[0]
     n_meshes = args["cb_same"].shape[0]
+    opt_off = np.asarray(args["opt_off"])
+    g_mesh = np.asarray(args["g_mesh"])
+    if (len(opt_off) != n_meshes + 1 or int(opt_off[0]) != 0 or int(opt_off[-1]) != n_opts
+            or np.any(np.diff(opt_off) < 0)):
+        raise ValueError("dp_sweep: opt_off must partition the options by mesh")
+    if G >= 1 and (np.any(g_mesh[1:] < 0) or np.any(g_mesh[1:] >= n_meshes)):
+        raise ValueError("dp_sweep: g_mesh out of range")
     dt = DeviceTables(L, G, n_opts, n_meshes).load_dense(args, s_max)
-    _cache.clear()
+    if int(dt.counters()[10]):
+        raise ValueError(
+            "dp_sweep: unsupported remaining-device encoding (an option with no "
+            "device, or a successor state whose boundary row depends on the "
+            "caller; see hapt_tables_finalize in include/hapt_b200.h)")
     _cache[key] = (dt, dict(args), Sweeper(dt))
-    return dt
+    while len(_cache) > _CACHE_MAX:
+        _cache.popitem(last=False)
+    return dt, _cache[key][2]
 
 
 def dp_sweep(t_max, t_tab, mp_tab, ma_tab, opt_cap, opt_mesh, opt_devs, opt_off, cb_same,
@@ -80,11 +97,10 @@ def dp_sweep(t_max, t_tab, mp_tab, ma_tab, opt_cap, opt_mesh, opt_devs, opt_off,
     args = dict(t_tab=t_tab, mp_tab=mp_tab, ma_tab=ma_tab, opt_cap=opt_cap, opt_mesh=opt_mesh,
                 opt_devs=opt_devs, opt_off=opt_off, cb_same=cb_same, cb_next=cb_next,
                 g_mesh=g_mesh, g_avail=g_avail, span_off=span_off, span_items=span_items)
-    _check_encoding(np.asarray(g_mesh), np.asarray(g_avail), np.asarray(opt_off))
-    dt = _device_tables(args, s_max)
-    sw = next(iter(_cache.values()))[2]
-    F, N, bpi, bpo = sw.full_tables(float(t_max))
-    return F.cpu().numpy(), N.cpu().numpy(), bpi.cpu().numpy(), bpo.cpu().numpy()
+    with _lock:
+        _dt, sw = _entry(args, s_max)  # _dt keeps the tables alive for the call
+        F, N, bpi, bpo = sw.full_tables(float(t_max))
+        return F.cpu().numpy(), N.cpu().numpy(), bpi.cpu().numpy(), bpo.cpu().numpy()
 
 
 __all__ = ["dp_sweep", "BACKEND"]

@@ -439,19 +439,44 @@ __global__ void k_srank(hapt_tables t) {
 // g >= g' - g_avail[g'], so: g strictly inside mesh r (g_mesh[g+1] == g_mesh[g])
 // -> same mesh, cb_same[r]; g the full budget of its mesh, or g = 0 -> the
 // caller left mesh r = g_mesh[g+1] -> cb_next[r]; g = G has no caller.
+//
+// Stated for any (g_mesh, g_avail) encoding a drop-in caller may pass
+// (_dp.pyx:58-77): every caller g > g2 whose mesh r = g_mesh[g] has an option
+// of exactly g - g2 <= g_avail[g] devices reads cb_same[r] if g2 >= 1 and
+// g_mesh[g2] == r, else cb_next[r].  The DP hoists c into the successor
+// table, so the row must not depend on the caller; DpTables' encoding
+// (meshes consumed in order) always satisfies this and gives the rule above.
+// A state with callers that disagree raises counters[10] (the host refuses
+// the encoding); a state with no caller gets -1 (its entry is never read).
 __global__ void k_gcrow(hapt_tables t) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g > t.G) return;
+  const int g2 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g2 > t.G) return;
   const int nm = t.n_meshes;
-  int row;
-  if (g == t.G) {
-    row = -1;
-  } else if (g >= 1 && t.g_mesh[g + 1] == t.g_mesh[g]) {
-    row = t.g_mesh[g];
-  } else {
-    row = nm + t.g_mesh[g + 1];
+  int row = -1;
+  bool conflict = false;
+  for (int g = g2 + 1; g <= t.G; ++g) {
+    const int r = t.g_mesh[g], devs = g - g2;
+    if (r < 0 || r >= nm) {
+      conflict = true;
+      continue;
+    }
+    if (devs > t.g_avail[g]) continue;
+    bool has = false;
+    for (int o = t.opt_off[r]; o < t.opt_off[r + 1] && !has; ++o) has = t.opt_devs[o] == devs;
+    if (!has) continue;
+    const int rr = (g2 >= 1 && t.g_mesh[g2] == r) ? r : nm + r;
+    if (row < 0) row = rr;
+    else conflict |= row != rr;
   }
-  t.g_crow[g] = row;
+  t.g_crow[g2] = row;
+  if (conflict) t.counters[10] = 1;
+}
+
+// Encoding checks the DP relies on besides g_crow: every option uses at least
+// one device (cells with fewer devices than remaining stages are skipped).
+__global__ void k_encoding(hapt_tables t) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o < t.n_opts && t.opt_devs[o] < 1) t.counters[10] = 1;
 }
 
 }  // namespace
@@ -488,6 +513,8 @@ int finalize_impl(hapt_tables *tp, cudaStream_t st) {
   k_pool_decode<<<grid_for(y.pool_cap, 256), 256, 0, st>>>(t, uniq, num_unique); ::hapt::note_launch();
   k_prank<<<grid_for(y.nnz_cap, 256), 256, 0, st>>>(t); ::hapt::note_launch();
   k_srank<<<grid_for(rows * 32, 256), 256, 0, st>>>(t); ::hapt::note_launch();
+  HAPT_CUDA(cudaMemsetAsync(&t.counters[10], 0, 8, st));
+  k_encoding<<<grid_for(t.n_opts, 128), 128, 0, st>>>(t); ::hapt::note_launch();
   k_gcrow<<<grid_for(t.G + 1, 128), 128, 0, st>>>(t); ::hapt::note_launch();
   HAPT_LAUNCHED("finalize");
   return HAPT_OK;

@@ -92,3 +92,43 @@ def assert_plan_equal(got: dict, ref: dict, stats: bool = True) -> None:
 
 def isinf(x) -> bool:
     return isinstance(x, float) and math.isinf(x)
+
+
+REF = os.path.join(os.path.dirname(HERE), "oracle", "_ref")
+
+
+def reference_meshpipe():
+    """The unmodified reference package (oracle/_ref, built by oracle/Makefile)
+    or None when it is not built.  Test infrastructure only."""
+    import sys
+
+    if not os.path.isdir(os.path.join(REF, "meshpipe")):
+        return None
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import meshpipe  # noqa: F401
+    import meshpipe.planner  # noqa: F401
+
+    return meshpipe
+
+
+def ref_types(inst: dict):
+    """Golden dict -> the reference's own (store, costs, B, eps): reference
+    LayerSequence / ClusterSpec / CostModel, reference build_store."""
+    from meshpipe.cluster import ClusterSpec as RC, DeviceMesh as RM
+    from meshpipe.model_graph import Layer as RL, LayerSequence as RS
+    from meshpipe.profiling import CostModel as RCM, boundary_costs as rbc, build_store as rbs
+
+    lay = inst["layers"]
+    layers = RS(tuple(RL(i, i + 1, lay["flops"][i], lay["param_bytes"][i],
+                         lay["boundary_bytes"][i], tuple(lay["signature"][i]))
+                      for i in range(len(lay["flops"]))), ())
+    meshes = [RM(m["id"], m["hosts"], m["devices_per_host"], m["peak_flops"], m["mem_device"],
+                 m["intra_host_bw"], m["inter_host_bw"]) for m in inst["cluster"]["meshes"]]
+    cb = inst["cluster"]["cross_bw"]
+    if isinstance(cb, list):
+        cb = {(a, b): v for a, b, v in cb}
+    cl = RC(meshes, cross_bw=cb, cross_latency=inst["cluster"]["cross_latency"])
+    store = rbs(layers, cl, RCM(**inst["model"]), imbalance_ratio=float(inst["imbalance_ratio"]),
+                dedup=inst.get("dedup", True))
+    return store, rbc(layers, cl), inst["num_microbatches"], inst["epsilon"]

@@ -122,3 +122,31 @@ def test_launch_counts_kinds_and_errors():
     assert (cl[:, 0] == S).all()
     eg, _ = launch_counts_batch(t, np.zeros_like(t), c, kind="eager")
     assert (eg[:, 0] == 2 * S - 1).all()
+
+
+def test_config_e_benchmark_scale_equals_oracle():
+    """The bench's config E workload at full size: all 10^6 plans through
+    the same PlanBatch.counts + PlanBatch.simulate calls bench.py times
+    (adaptive counts, B = 128), every launch count and every makespan
+    compared bit for bit with the oracle's explicit-DAG Kahn simulator
+    (oracle_config_e_batch: adaptive_counts + build_dag + simulate per plan)."""
+    import torch
+
+    from paper_2509_24859_b200.simulation import PlanBatch
+    from paper_2509_24859_b200.workloads import config_e
+
+    n = 1_000_000
+    f, b, c, S = config_e(n)
+    batch = PlanBatch(f, b, c, stage_counts=S, device=torch.device("cuda", 0))
+    counts, status = batch.counts(0.05, "adaptive")
+    mk, st = batch.simulate(counts, 128, ring_depth=3 * 8 + 2)
+    assert (status == 0).all().item() and (st == 0).all().item()
+    ocounts, ostatus, omk = O.config_e_batch(f, b, c, S, B=128, epsilon=0.05)
+    assert (ostatus == 0).all()
+    dense = np.zeros((n, 8), dtype=np.int32)
+    mask = np.arange(8)[None, :] < S[:, None]
+    dense[mask] = counts.cpu().numpy()
+    assert np.array_equal(dense, ocounts)
+    got = mk.cpu().numpy()
+    bad = np.flatnonzero(got != omk)
+    assert bad.size == 0, (bad[:10], got[bad[:10]], omk[bad[:10]])

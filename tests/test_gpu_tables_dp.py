@@ -146,3 +146,28 @@ def test_every_kernel_variant_equals_reference(env):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                        env={**os.environ, **env}, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("name", ["D2", "D3"])
+def test_full_pool_strided_sample_equals_reference(name):
+    """D2 / D3 full pools (7,019 / 15,925 candidates, the bench's per_config
+    lines): the batched sweep of the WHOLE pool, checked at a strided sample
+    of >= 300 candidates plus the neighbourhoods of the first feasible
+    candidate and of search()'s winner, against the reference's own
+    per-candidate dp_sweep + _extract_plan (tests/golden/make_golden_sample.py)."""
+    from paper_2509_24859_b200.planner import sweep_pool
+
+    inst = load_json(name)
+    smp = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "instances",
+                               f"{name}_sample.npz"))
+    store, costs, cluster, B, eps = build(inst)
+    pool, tstar, best_s, states, winner = sweep_pool(store, costs, B)
+    idx = smp["idx"]
+    assert len(idx) >= 300
+    assert np.array_equal(pool[idx], smp["tmax"])
+    assert np.array_equal(tstar[idx], smp["tstar"])
+    assert np.array_equal(best_s[idx], smp["best_s"])
+    assert np.array_equal(states[idx], smp["states"])
+    ff = int(smp["first_feasible"])
+    assert np.isfinite(tstar[ff]) and not np.isfinite(tstar[ff - 1])
+    assert pool[winner] == expected(name)["plan"]["t_max"]

@@ -34,13 +34,21 @@ namespace hapt {
 namespace {
 
 #ifdef HAPT_COUNT_WORK
-__device__ unsigned long long g_work[4];  // executed / admissible / improving
+__device__ unsigned long long g_work[8];  // executed / admissible / improving lane-transitions,
+                                          // -, cell-tasks, empty cells, all-infinite cells, staged chunks
 #endif
 #ifndef HAPT_KWARPS
 #define HAPT_KWARPS 4
 #endif
 constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
+#ifndef HAPT_CHUNK
+#define HAPT_CHUNK 1
+#endif
+constexpr int kChunk = HAPT_CHUNK;
+#ifndef HAPT_WIN_MINLEN
+#define HAPT_WIN_MINLEN 1  // window hull also bounded by each option's shortest span
+#endif  // window cells of one (group, state) per relax warp
 #ifndef HAPT_RELAX_WARPLOOP
 #define HAPT_RELAX_WARPLOOP 1  // 0: units of kWarps cells with block barriers (v14)
 #endif
@@ -114,9 +122,12 @@ struct Batch {
   int2 *irange[3];     // [n_groups][G+1] (min, max) split i whose successor entry
                        // (state g) is finite for some candidate of the group;
                        // layer s reads [(s-1)%3], writes [s%3], resets [(s+1)%3]
-  uint16_t *maxlen;    // [n_groups][n_opts] longest admissible span of an option
-  uint32_t *clist;     // [n_groups][ccap] (g << 16 | k) of the cells inside the
-                       // current layer's windows, group-local compact order
+  uint32_t *spanlen;   // [n_groups][n_opts] shortest << 16 | longest admissible span
+                       // length of an option (before the group's cut)
+  uint16_t *winhi;     // [n_groups][G+1] last k of state g's window (dp_window)
+  uint32_t *clist;     // [n_groups][ccap] (g << 16 | k0): chunks of up to kChunk
+                       // cells k0.. of state g inside the current layer's windows,
+                       // group-local compact order
   size_t ccap;         // L*G >= cells of any layer
   int32_t *gtot;       // [n_groups] window cells per group, reserved by
                        // dp_window's warps (zero between windowed layers)
@@ -138,7 +149,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], maxlen, clist, gtot, goff, ticket, gmeta, spart, H0,
+  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], spanlen, winhi, clist, gtot, goff, ticket, gmeta, spart, H0,
       H1, K0, K1, Hm0, Hm1, total;
 };
 
@@ -157,7 +168,8 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
     w.ir[j] = cur;
     cur += align_up(ng * (t->G + 1) * sizeof(int2));
   }
-  w.maxlen = cur; cur += align_up(ng * t->n_opts * 2);
+  w.spanlen = cur; cur += align_up(ng * t->n_opts * 4);
+  w.winhi = cur; cur += align_up(ng * (t->G + 1) * 2);
   w.clist = cur; cur += align_up(ng * (size_t)t->L * t->G * 4);
   w.gtot = cur; cur += align_up(ng * 4);
   w.goff = cur; cur += align_up((ng + 1) * 4);
@@ -190,6 +202,7 @@ __global__ void dp_prep(Batch b) {
   pdl_wait();
   pdl_trigger();
   __shared__ int s_gmax;
+  __shared__ int s_mn[2048], s_mx[2048];  // n_opts < 2048 (hapt_tables_init)
   const int group = blockIdx.x;
   const int cw = b.cw;
   if (threadIdx.x == 0) s_gmax = 0;
@@ -230,6 +243,14 @@ __global__ void dp_prep(Batch b) {
   // suffix-min ranks are non-decreasing along a row: first entry no candidate
   // of this group can accept (prank >= srank >= max tcnt) ends the row's scan
   const int gm = s_gmax;
+  // shortest / longest admissible span (before the cut) of each option, for
+  // dp_window: entries are in ascending span end, so the row's first entry
+  // is its shortest and the last one before the cut its longest
+  for (int o = threadIdx.x; o < b.n_opts; o += blockDim.x) {
+    s_mn[o] = 0xffff;
+    s_mx[o] = 0;
+  }
+  __syncthreads();
   for (int row = threadIdx.x; row < b.rows; row += blockDim.x) {
     const int beg = b.span_off[row], end = b.span_off[row + 1];
     int lo = beg, hi = end;
@@ -238,22 +259,16 @@ __global__ void dp_prep(Batch b) {
       if (b.span_srank[mid] < gm) lo = mid + 1; else hi = mid;
     }
     b.cut_sr[(size_t)group * b.rows + row] = (uint16_t)(lo - beg);
+    if (lo > beg) {
+      const int o = row / (b.L + 2), k = row - o * (b.L + 2);
+      atomicMin(&s_mn[o], (int)b.spans[beg].i - k + 1);
+      atomicMax(&s_mx[o], (int)b.spans[lo - 1].i - k + 1);
+    }
   }
   __syncthreads();
-  // longest admissible span (before the cut) of each option, for dp_window
-  for (int o = threadIdx.x; o < b.n_opts; o += blockDim.x) {
-    int ml = 0;
-    for (int k = 1; k <= b.L; ++k) {
-      const int row = o * (b.L + 2) + k;
-      const int cut = b.cut_sr[(size_t)group * b.rows + row];
-      if (cut > 0) {
-        // entries are in ascending span end: the last admissible one is the longest
-        const int beg = b.span_off[row];
-        ml = max(ml, (int)b.spans[beg + cut - 1].i - k + 1);
-      }
-    }
-    b.maxlen[(size_t)group * b.n_opts + o] = (uint16_t)ml;
-  }
+  for (int o = threadIdx.x; o < b.n_opts; o += blockDim.x)
+    b.spanlen[(size_t)group * b.n_opts + o] =
+        s_mx[o] ? ((unsigned)s_mn[o] << 16) | (unsigned)s_mx[o] : 0u;
   // the launch-bound increment of every boundary entry for every candidate:
   // kk = (ceil(2c/t_max) + 1) + N (_dp.pyx:82, same association); c > t_max
   // skips the transition (_dp.pyx:76-78) -> 0xFF
@@ -302,62 +317,54 @@ __global__ void dp_prep(Batch b) {
 // reserves its states' cells in the group's list with one atomic (the order
 // of states in the list does not matter: cells are independent), and the
 // last block turns the group totals into goff.
-constexpr int kWinBlock = 64;
-__global__ void __launch_bounds__(kWinBlock) dp_window(Batch b, int s) {
+constexpr int kWinWarps = 4;  // states per dp_window block (one warp each)
+__global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
   pdl_wait();
   pdl_trigger();
   const int group = blockIdx.y;
   const int L = b.L, G = b.G, imax = L - s + 1;
   const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x * kWinBlock + threadIdx.x;
+  const int g = blockIdx.x * kWinWarps + (threadIdx.x >> 5);
+  // one warp per state g, lane j = option gm.x + j (+32, ... for larger
+  // meshes): every option's loads are independent, the hull is a warp min/max
   int klo = 0x7fff, khi = 0;
   if (g <= G && g >= s) {
-    const int r = b.g_mesh[g], avail = b.g_avail[g];
-    const int oa = b.opt_off[r], ob = b.opt_off[r + 1];
-    // four options at a time with independent loads (the per-thread chain
-    // of dependent loads is this kernel's whole cost)
-    for (int o0 = oa; o0 < ob; o0 += 4) {
-      int2 fr[4];
-      int ml[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int o = o0 + u;
-        fr[u] = make_int2(1, 0);
-        ml[u] = 0;
-        if (o < ob) {
-          const int devs = b.opt_devs[o], g2 = g - devs;
-          if (devs <= avail && g2 >= s - 1) {
-            fr[u] = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
-            ml[u] = b.maxlen[(size_t)group * b.n_opts + o];
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int hi = min(imax, fr[u].y);
-        if (fr[u].x > hi || ml[u] == 0) continue;
-        klo = min(klo, max(1, fr[u].x - ml[u] + 1));
-        khi = max(khi, hi);
-      }
+    const int4 gm = b.gmeta[g];
+    for (int j = lane; j < gm.y; j += 32) {
+      const int o = gm.x + j;
+      const int devs = __ldg(b.opt_devs + o), g2 = g - devs;
+      if (devs > gm.z || g2 < s - 1) continue;
+      const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
+      const uint32_t ml = __ldg(b.spanlen + (size_t)group * b.n_opts + o);
+      // option o reaches a finite successor from cell k only through spans
+      // (k, i) with i in [fr.x, min(fr.y, L-s+1)] and admissible length
+      // i-k+1 in [minlen_o, maxlen_o]
+      const int mx = (int)(ml & 0xffffu), mn = (int)(ml >> 16);
+      const int hi = min(imax, fr.y);
+      if (fr.x > hi || mx == 0) continue;
+      klo = min(klo, max(1, fr.x - mx + 1));
+#if HAPT_WIN_MINLEN
+      khi = max(khi, hi - mn + 1);
+#else
+      (void)mn;
+      khi = max(khi, hi);
+#endif
     }
   }
-  const int n = khi >= klo ? khi - klo + 1 : 0;
-  // warp-exclusive prefix and one reservation per warp
-  int incl = n;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += v;
-  }
-  const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-  int base = 0;
-  int32_t *cnt = b.gtot + group;
-  if (lane == 31 && wtot > 0) base = atomicAdd(cnt, wtot);
-  base = __shfl_sync(0xffffffffu, base, 31);
+  klo = __reduce_min_sync(0xffffffffu, klo);
+  khi = __reduce_max_sync(0xffffffffu, khi);
+  // chunks of up to kChunk consecutive k; winhi bounds the last chunk
+  const int n = khi >= klo ? (khi - klo + kChunk) / kChunk : 0;
   if (g <= G) {
-    uint32_t *cl = b.clist + (size_t)group * b.ccap + base + (incl - n);
-    for (int t = 0; t < n; ++t) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t);
-    b.irange[(s + 1) % 3][(size_t)group * (G + 1) + g] = make_int2(0x7fffffff, -1);
+    int base = 0;
+    if (lane == 0 && n > 0) base = atomicAdd(b.gtot + group, n);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    uint32_t *cl = b.clist + (size_t)group * b.ccap + base;
+    for (int t = lane; t < n; t += 32) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t * kChunk);
+    if (lane == 0) {
+      if (kChunk > 1) b.winhi[(size_t)group * (G + 1) + g] = (uint16_t)khi;
+      b.irange[(s + 1) % 3][(size_t)group * (G + 1) + g] = make_int2(0x7fffffff, -1);
+    }
   }
   __shared__ bool last;
   __syncthreads();
@@ -436,10 +443,10 @@ __device__ __forceinline__ void load_k(const char *p, int (&k)[CPL]) {
 template <bool WITH_KK, int CPL>
 __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
                                               const uint16_t *__restrict__ skm, int n,
-                                              const unsigned (&cnt2)[CPL],
+                                              const unsigned (&cnt)[CPL],
                                               const char *__restrict__ Hb,
                                               const char *__restrict__ Kb, double (&bv)[CPL],
-                                              unsigned (&bw2)[CPL], unsigned (&bw3)[CPL]) {
+                                              unsigned (&bw3)[CPL]) {
   constexpr int U = Unroll<CPL>::value;
   for (int u = 0; u < n; u += U) {
     int4 ex[U];
@@ -460,15 +467,14 @@ __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
         const double v = __dadd_rn(tt, h[q][c]);  // tt + (2c + F)  (_dp.pyx:85)
 #ifdef HAPT_COUNT_WORK  // instrumented build only (tools/work_counts.py)
         if (u + q < n) {
-          const bool adm = (unsigned)ex[q].z < cnt2[c] && h[q][c] != kInf;
+          const bool adm = (unsigned)ex[q].z < cnt[c] && h[q][c] != kInf;
           atomicAdd(&g_work[0], 1ull);
           if (adm) atomicAdd(&g_work[1], 1ull);
           if (adm && v < bv[c]) atomicAdd(&g_work[2], 1ull);
         }
 #endif
-        if ((unsigned)ex[q].z < cnt2[c] && (!WITH_KK || kk[q][c] <= km) && v < bv[c]) {
+        if ((unsigned)ex[q].z < cnt[c] && (!WITH_KK || kk[q][c] <= km) && v < bv[c]) {
           bv[c] = v;
-          bw2[c] = (unsigned)ex[q].z;
           bw3[c] = (unsigned)ex[q].w;
         }
       }
@@ -476,21 +482,75 @@ __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
   }
 }
 
+// Per-lane option data of state g at layer s that does not depend on the
+// cell's k: lane j holds option o0 + c0 + j of mesh g_mesh[g].  Computed once
+// per chunk of cells of one (group, g) and reused by every cell of the chunk
+// (the opt_devs -> irange part of the per-cell dependent-load chain).
+struct OptLane {
+  int2 fr;    // finite-successor split range of g2 = g - devs (empty: not admissible)
+  int hbase;  // g2 * (L+1): successor row of g2
+};
+
+__device__ __forceinline__ OptLane opt_lane(const Batch &b, int s, int group, int g, int o,
+                                            int avail, bool valid) {
+  OptLane ol;
+  ol.fr = make_int2(1, 0);
+  ol.hbase = 0;
+  if (valid) {
+    const int devs = __ldg(b.opt_devs + o), g2 = g - devs;
+    if (devs <= avail && g2 >= s - 1) {
+      // admissible splits: inside the range where state g2's successor entry
+      // is finite for some candidate of the group (the rest are ones the
+      // reference skips for all these candidates: fc == inf)
+      ol.fr = b.irange[(s - 1) % 3][(size_t)group * (b.G + 1) + g2];
+      ol.hbase = g2 * (b.L + 1);
+    }
+  }
+  return ol;
+}
+
+// Option of a cell's winner, for backpointers only (the transition loop
+// tracks just the winner's successor).  The winner is the first entry in the
+// reference's order (o ascending, then i) with the minimum value; every entry
+// through the winning successor (g2 = g - devs, split i) shares its H, so the
+// winner's option is the first option of the mesh with devs devices whose
+// span (k, i) is admissible for this candidate (tt <= t_max, KK <= kmax) and
+// whose value tt + H equals the best (_dp.pyx:58-91, strict '<' update).
+__device__ __noinline__ int winner_option(const int32_t *opt_devs, const int32_t *span_off,
+                                          const hapt_span *spans, int L, int k, int devs, int i,
+                                          double best, unsigned cnt, int kk, double h, int o0,
+                                          int nopt) {
+  for (int o = o0; o < o0 + nopt; ++o) {
+    if (opt_devs[o] != devs) continue;
+    const int row = o * (L + 2) + k;
+    int lo = span_off[row], hi = span_off[row + 1];
+    while (lo < hi) {  // entries ascend in span end i
+      const int mid = (lo + hi) >> 1;
+      if ((int)spans[mid].i < i) lo = mid + 1; else hi = mid;
+    }
+    if (lo == span_off[row + 1] || (int)spans[lo].i != i) continue;
+    const hapt_span e = spans[lo];
+    if ((unsigned)e.prank < cnt && kk <= (int)e.kmax && __dadd_rn(e.tt, h) == best) return o;
+  }
+  return -1;  // unreachable for a recorded winner
+}
+
 // One DP cell (k, g) of layer s for the 32*CPL candidates of `group`, executed
 // by one warp: fin[c] = whether the cell is finite for candidate c; writes the
 // successor entry of layer s+1 and, for a finite entry, widens irange.
+// ol0: opt_lane() of the mesh's first 32 options (lane j = option o0 + j).
 template <int CPL>
 __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int k, int g,
                                            int lane, int4 *__restrict__ stage_e,
-                                           uint16_t *__restrict__ stage_k, int (&fin)[CPL]) {
+                                           uint16_t *__restrict__ stage_k, int (&fin)[CPL],
+                                           const int4 gm, const OptLane &ol0) {
   constexpr int CW = 32 * CPL;
   const int L = b.L, G = b.G;
   const int cand0 = group * CW + lane * CPL;
-  unsigned cnt2[CPL];
+  unsigned cnt[CPL];  // #pool values <= t_max: tt <= t_max <=> prank < cnt
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) cnt2[c] = (unsigned)b.tcnt[cand0 + c] << 11;
+  for (int c = 0; c < CPL; ++c) cnt[c] = (unsigned)b.tcnt[cand0 + c];
   const int imax = L - s + 1;
-  const int4 gm = b.gmeta[g];
   const int o0 = gm.x, nopt = gm.y, avail = gm.z;
   const size_t gbase = (size_t)group * b.hg;
   const double *Hg = b.H[(s - 1) & 1] + gbase * CW + lane * CPL;
@@ -498,52 +558,40 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   const char *Hb = reinterpret_cast<const char *>(Hg);
   const char *Kb = reinterpret_cast<const char *>(Kg);
   double bv[CPL];
-  unsigned bw2[CPL], bw3[CPL];
+  unsigned bw3[CPL];  // successor byte offset of the winner (its option: winner_option)
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     bv[c] = kInf;
-    bw2[c] = ~0u;
     bw3[c] = 0;
   }
   // options of mesh r, 32 at a time (a mesh rarely has more than 32 submesh
   // shapes); rows are visited in ascending option order
   for (int c0 = 0; c0 < nopt; c0 += 32) {
     const int nch = min(32, nopt - c0);
-    // lane j: admissible entries of option o0+c0+j's row (k) at this layer
-    int len = 0, beg = 0, hbase = 0;
+    const int o = o0 + c0 + lane;
+    const OptLane ol = c0 == 0 ? ol0 : opt_lane(b, s, group, g, o, avail, lane < nch);
+    // lane j: admissible entries of option o's row (k) at this layer
+    int len = 0, beg = 0;
     bool needkk = false;
-    if (lane < nch) {
-      const int o = o0 + c0 + lane;
+    const int lo_i = max(k, ol.fr.x), hi_i = min(imax, ol.fr.y);
+    if (lane < nch && lo_i <= hi_i) {
       const int row = o * (L + 2) + k;
-      // the row's own metadata does not depend on the successor range:
-      // loaded up front, beside the opt_devs -> irange -> row_pos chain
-      const int devs = __ldg(b.opt_devs + o);
+      // admissible splits also end at i <= L-s+1 (later successors are
+      // provably infinite) and before the group's suffix-rank cut
       const int cut = __ldg(b.cut_sr + (size_t)group * b.rows + row);
       const int soff = __ldg(b.span_off + row);
       const int kmin = __ldg(b.row_kmin + row);
-      const int g2 = g - devs;
-      if (devs <= avail && g2 >= s - 1) {
-        // admissible splits: i <= L-s+1 (later successors are provably
-        // infinite), inside the range where state g2's successor entry is
-        // finite for some candidate of the group, and before the group's
-        // suffix-rank cut -- every skipped entry is one the reference
-        // skips for all these candidates (fc == inf or tt > t_max)
-        const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
-        const int lo_i = max(k, fr.x), hi_i = min(imax, fr.y);
-        if (lo_i <= hi_i) {
-          const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
-          const int a = __ldg(pos + lo_i - 1);
-          const int z = min((int)__ldg(pos + hi_i), cut);
-          beg = soff + a;
-          len = max(0, z - a);
-        }
-        hbase = g2 * (L + 1);
-        // KK <= 3s at layer s: ceil(2c/t_max) <= 2 and N grows by <= 3 per
-        // stage, so a row whose thresholds are all >= 3s cannot fail the
-        // memory mask (_dp.pyx:83)
-        needkk = len > 0 && kmin < 3 * s;
-      }
+      const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
+      const int a = __ldg(pos + lo_i - 1);
+      const int z = min((int)__ldg(pos + hi_i), cut);
+      beg = soff + a;
+      len = max(0, z - a);
+      // KK <= 3s at layer s: ceil(2c/t_max) <= 2 and N grows by <= 3 per
+      // stage, so a row whose thresholds are all >= 3s cannot fail the
+      // memory mask (_dp.pyx:83)
+      needkk = len > 0 && kmin < 3 * s;
     }
+    const int hbase = ol.hbase;
     int incl = len;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -552,6 +600,13 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     }
     const int T = __shfl_sync(0xffffffffu, incl, 31);
     const int start = incl - len;
+#ifdef HAPT_COUNT_WORK
+    if (lane == 0 && c0 == 0) {
+      atomicAdd(&g_work[4], 1ull);
+      if (T == 0 && nopt <= 32) atomicAdd(&g_work[5], 1ull);
+      atomicAdd(&g_work[7], (unsigned long long)((T + 31) / 32));
+    }
+#endif
     const bool anykk = __any_sync(0xffffffffu, needkk);
     const double *Hm = b.Hmin[(s - 1) & 1] + gbase;
     for (int r0 = 0; r0 < T; r0 += 32) {
@@ -590,9 +645,8 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
         const int succ = oh + (x.w & 0xffff);
         lb = __dadd_rn(__hiloint2double(x.y, x.x), __ldg(Hm + succ));
         keep = lb < bmax;
-        const unsigned w2 =
-            x.z == 0x7fffffff ? ~0u : ((unsigned)x.z << 11) | (unsigned)(o0 + c0 + j);
-        se = make_int4(x.x, x.y, (int)w2, succ * (256 * CPL));
+        // w2 = pool rank (INT32_MAX for a non-finite t: never below a count)
+        se = make_int4(x.x, x.y, x.z, succ * (256 * CPL));
         sk = (uint16_t)((unsigned)x.w >> 16);
       }
       // Best-first probe: evaluate the kept entry with the smallest bound
@@ -619,7 +673,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           double m = bv[c];
-          if (pz < cnt2[c] && (!anykk || kp[c] <= pk)) m = fmin(m, __dadd_rn(pt, hp[c]));
+          if (pz < cnt[c] && (!anykk || kp[c] <= pk)) m = fmin(m, __dadd_rn(pt, hp[c]));
           mh = max(mh, (unsigned)__double2hiint(m));
         }
         mh = __reduce_max_sync(0xffffffffu, mh);
@@ -639,9 +693,9 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       }
       __syncwarp();
       if (anykk)
-        relax_entries<true, CPL>(stage_e, stage_k, n, cnt2, Hb, Kb, bv, bw2, bw3);
+        relax_entries<true, CPL>(stage_e, stage_k, n, cnt, Hb, Kb, bv, bw3);
       else
-        relax_entries<false, CPL>(stage_e, stage_k, n, cnt2, Hb, Kb, bv, bw2, bw3);
+        relax_entries<false, CPL>(stage_e, stage_k, n, cnt, Hb, Kb, bv, bw3);
       __syncwarp();
     }
   }
@@ -655,11 +709,14 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   {
     bool any = false;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) any |= bw2[c] != ~0u;
+    for (int c = 0; c < CPL; ++c) any |= bv[c] < kInf;
     if (!__any_sync(0xffffffffu, any)) {
 #pragma unroll
       for (int c = 0; c < CPL; ++c) fin[c] = 0;
       if (lane == 0) b.Hmin[s & 1][hm_idx] = kInf;
+#ifdef HAPT_COUNT_WORK
+      if (lane == 0) atomicAdd(&g_work[6], 1ull);
+#endif
       return;
     }
   }
@@ -673,9 +730,16 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   // warp-uniform: backpointers / F / N are only recorded when a caller asked
   const bool want_bp = b.full.bp_packed != nullptr || b.full.bp_o != nullptr;
   const bool top = k == 1 && g == G;
+  // the CPL launch-bound increments of this lane in one load
+  unsigned kcw = 0xFFFFFFFFu;
+  if (crow >= 0) {
+    if constexpr (CPL == 4) kcw = __ldg(reinterpret_cast<const unsigned *>(kcp));
+    else if constexpr (CPL == 2) kcw = __ldg(reinterpret_cast<const uint16_t *>(kcp));
+    else kcw = __ldg(kcp);
+  }
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
-    fin[c] = bw2[c] != ~0u;
+    fin[c] = bv[c] < kInf;
     const double best = bv[c];
     const unsigned boff = bw3[c] / (256u * CPL);
     // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
@@ -686,9 +750,9 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
     }
     if (want_bp && fin[c] && cand < b.n_cand) {
-      const int bo = (int)(bw2[c] & 2047u);
-      // split i of the winner: its successor offset minus the row of g2 = g - devs
-      const int bi = (int)boff - (g - b.opt_devs[bo]) * (L + 1);
+      const int g2 = (int)boff / (L + 1), bi = (int)boff - g2 * (L + 1);
+      const int bo = winner_option(b.opt_devs, b.span_off, b.spans, L, k, g - g2, bi, best,
+                                   cnt[c], bkk, __ldg(Hg + (size_t)boff * CW + c), gm.x, gm.y);
       const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
       if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
       if (b.full.bp_o) {
@@ -702,7 +766,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     // H = 2c + F, KK = (ceil(2c/t_max) + 1) + N, or +inf if c > t_max
     hn[c] = kInf;
     kn[c] = 0;
-    const int kcv = crow >= 0 ? (int)kcp[c] : 0xFF;
+    const int kcv = crow >= 0 ? (int)((kcw >> (8 * c)) & 0xFFu) : 0xFF;
     if (fin[c] && kcv != 0xFF) {
       hn[c] = __dadd_rn(c2, best);
       kn[c] = kcv + bkk;
@@ -720,10 +784,20 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   if (lane == 0) b.Hmin[s & 1][hm_idx] = __hiloint2double((int)hh, 0);
   const bool wfin = __any_sync(0xffffffffu, anyfin);
   if (wfin) {  // otherwise Hmin = +inf already shields the slots (see above)
+    double *ho = b.H[s & 1] + o_idx;
+    uint16_t *ko = b.K[s & 1] + o_idx;
+    if constexpr (CPL == 1) {
+      ho[0] = hn[0];
+      ko[0] = (uint16_t)kn[0];
+    } else {
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      b.H[s & 1][o_idx + c] = hn[c];
-      b.K[s & 1][o_idx + c] = (uint16_t)kn[c];
+      for (int c = 0; c < CPL; c += 2)
+        reinterpret_cast<double2 *>(ho)[c / 2] = make_double2(hn[c], hn[c + 1]);
+      if constexpr (CPL == 2)
+        *reinterpret_cast<unsigned *>(ko) = (unsigned)kn[0] | ((unsigned)kn[1] << 16);
+      else
+        *reinterpret_cast<uint2 *>(ko) = make_uint2((unsigned)kn[0] | ((unsigned)kn[1] << 16),
+                                                    (unsigned)kn[2] | ((unsigned)kn[3] << 16));
     }
   }
   if (wfin && lane == 0) {
@@ -756,7 +830,11 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   int fin[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) fin[c] = 0;
-  if (active) relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
+  if (active) {
+    const int4 gm = b.gmeta[g];
+    const OptLane ol0 = opt_lane(b, s, group, g, gm.x + lane, gm.z, lane < gm.y);
+    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm, ol0);
+  }
   if (blockIdx.x == 0) {  // the buffer layer s+1 writes: last read by layer s-1
     for (int x = threadIdx.x; x <= G; x += blockDim.x)
       b.irange[(s + 1) % 3][(size_t)group * (G + 1) + x] = make_int2(0x7fffffff, -1);
@@ -786,12 +864,13 @@ __device__ __forceinline__ int find_group(const int32_t *__restrict__ goff, int 
 }
 
 // Windowed layers: only the cells inside dp_window's windows, enumerated
-// compactly (group-major, then g, then k), one warp per cell over an
-// grid capped at 256 warps per SM that stride over the list -- no warp is
-// spent on a provably infinite cell.  Finite-cell counts go to one of kParts
-// counter copies (dp_states_reduce sums them) to avoid a same-address atomic
-// hot spot; by default (HAPT_RELAX_WARPLOOP) each warp keeps them in
-// registers and no warp waits at a block barrier for a slower one.
+// compactly as chunks of up to kChunk consecutive k of one (group, state g);
+// one warp per chunk over a grid capped at 256 warps per SM that strides
+// over the list -- no warp is spent on a provably infinite cell, and the
+// state's per-option data (opt_devs -> irange) is loaded once per chunk.
+// Finite-cell counts stay in registers while a warp's chunks stay in one
+// group and go to one of kParts counter copies (dp_states_reduce sums them)
+// when it changes, so no warp waits at a block barrier for a slower one.
 template <int CPL>
 __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     dp_relax_compact(Batch b, int s) {
@@ -802,15 +881,14 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   __shared__ uint16_t stage_k[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int total = b.goff[b.n_groups];
-#if HAPT_RELAX_WARPLOOP
-  // Barrier-free variant: every warp strides over the list on its own and
-  // keeps its finite-cell counts in registers while its cells stay in one
-  // group, flushing them to a counter copy when the group changes.
   uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
-  int cur = -1;
-  unsigned cnt[CPL];
+  // this warp's finite-cell counts of its current group (shared memory, not
+  // registers: the cell body is at the 64-register limit)
+  __shared__ unsigned s_cnt[kWarps][CW];
+  unsigned *cnt = &s_cnt[warp][lane * CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) cnt[c] = 0u;
+  int cur = -1;
   auto flush = [&](int grp) {
     uint32_t *dst = part + (size_t)grp * CW + lane * CPL;
     if constexpr (CPL == 1) {
@@ -832,61 +910,20 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
       cur = group;
     }
     const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
-    const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
-    int fin[CPL];
-    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
+    const int g = (int)(gk >> 16), k0 = (int)(gk & 0xffffu);
+    const int k1 = kChunk == 1 ? k0
+                               : min(k0 + kChunk - 1,
+                                     (int)__ldg(b.winhi + (size_t)group * (b.G + 1) + g));
+    const int4 gm = b.gmeta[g];
+    const OptLane ol0 = opt_lane(b, s, group, g, gm.x + lane, gm.z, lane < gm.y);
+    for (int k = k0; k <= k1; ++k) {
+      int fin[CPL];
+      relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm, ol0);
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) cnt[c] += fin[c] ? 1u : 0u;
+      for (int c = 0; c < CPL; ++c) cnt[c] += fin[c] ? 1u : 0u;
+    }
   }
   if (cur >= 0) flush(cur);
-#else
-  __shared__ unsigned s_cnt[2][CW];  // the unit's first group and the next
-  // units of kWarps consecutive cells, strided over the grid (the grid is
-  // the upper bound of the list, or fewer blocks that loop)
-  for (int idx0 = blockIdx.x * kWarps; idx0 < total; idx0 += gridDim.x * kWarps) {
-    for (int x = threadIdx.x; x < 2 * CW; x += blockDim.x) (&s_cnt[0][0])[x] = 0u;
-    __syncthreads();
-    const int group0 = find_group(b.goff, b.n_groups, idx0, lane);
-    const int idx = idx0 + warp;
-    if (idx < total) {
-      const int group = find_group(b.goff, b.n_groups, idx, lane);
-      const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
-      const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
-      int fin[CPL];
-      relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin);
-      const int slot = group - group0;  // a unit spans 8 cells: almost always 0 or 1
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        if (!fin[c]) continue;
-        if (slot < 2)
-          atomicAdd(&s_cnt[slot][lane * CPL + c], 1u);
-        else  // third group inside one unit (tiny groups): straight to a copy
-          atomicAdd(b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW +
-                        (size_t)group * CW + lane * CPL + c, 1u);
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {  // flush both slots
-      uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
-      for (int slot = 0; slot < 2 && group0 + slot < b.n_groups; ++slot) {
-        uint32_t *dst = part + (size_t)(group0 + slot) * CW + lane * CPL;
-        const unsigned *src = &s_cnt[slot][lane * CPL];
-        if constexpr (CPL == 1) {
-          if (src[0]) atomicAdd(dst, src[0]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < CPL; c += 2) {
-            const unsigned lo = src[c], hi = src[c + 1];
-            if (lo | hi)
-              atomicAdd(reinterpret_cast<unsigned long long *>(dst + c),
-                        (unsigned long long)lo | ((unsigned long long)hi << 32));
-          }
-        }
-      }
-    }
-    __syncthreads();  // s_cnt is reused by the next unit
-  }
-#endif
 }
 
 // states[cand] += sum of the kParts partial counters (padding lanes dropped)
@@ -1098,7 +1135,8 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.kc = (uint8_t *)(wb + w.kc);
   b.cb_rows = 2 * t->n_meshes;
   for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);
-  b.maxlen = (uint16_t *)(wb + w.maxlen);
+  b.spanlen = (uint32_t *)(wb + w.spanlen);
+  b.winhi = (uint16_t *)(wb + w.winhi);
   b.clist = (uint32_t *)(wb + w.clist);
   b.ccap = (size_t)t->L * t->G;
   b.gtot = (int32_t *)(wb + w.gtot);
@@ -1141,8 +1179,8 @@ int run_sweep(const Batch &b, cudaStream_t st) {
                                                           : 32768;
     const int use_window = cells * b.n_groups >= win_min;
     if (use_window) {
-      const dim3 wgrid((b.G + 1 + kWinBlock - 1) / kWinBlock, b.n_groups);
-      HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinBlock, st, pdl, b, s));
+      const dim3 wgrid((b.G + 1 + kWinWarps - 1) / kWinWarps, b.n_groups);
+      HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinWarps * 32, st, pdl, b, s));
       // the compact list's length is only known on the device: the grid is
       // its upper bound, capped at 256 warps per SM that loop over the cells
       // (measured: launching the bound's mostly empty blocks cost ~4 % of a
@@ -1371,7 +1409,7 @@ extern "C" int hapt_activated_pairs(const hapt_tables *t, const double *tmax, in
 // instrumented build only: cumulative transition counters of the DP loop
 extern "C" int hapt_debug_work(unsigned long long *out) {
   cudaDeviceSynchronize();
-  return cudaMemcpyFromSymbol(out, hapt::g_work, sizeof(unsigned long long) * 4) == cudaSuccess
+  return cudaMemcpyFromSymbol(out, hapt::g_work, sizeof(unsigned long long) * 8) == cudaSuccess
              ? HAPT_OK
              : HAPT_ECUDA;
 }

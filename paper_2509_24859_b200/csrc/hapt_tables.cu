@@ -553,10 +553,14 @@ extern "C" int hapt_tables_init(hapt_tables *t, void *buf, size_t buf_bytes, int
   t->n_opts = n_opts;
   t->n_meshes = n_meshes;
   t->s_max = L < G ? L : G;
+  // (G+1)(L+1) successor slots: a slot's byte offset (x 1 KB at 4 candidates
+  // per lane) is a 32-bit word of the staged transition, and the dense-layer
+  // cell decode is exact below 2^20 cells; n_opts: the per-option shared
+  // arrays of dp_prep; the CSR index itself is int32 (nnz < 2^31).
   if ((size_t)(G + 1) * (L + 1) >= (1u << 20) || n_opts >= 2048 ||
-      (size_t)n_opts * L * (L + 1) / 2 >= (1u << 21)) {
-    set_error("hapt_tables_init: (G+1)(L+1)=%zu or n_opts=%d exceeds the packed transition key",
-              (size_t)(G + 1) * (L + 1), n_opts);
+      (size_t)n_opts * L * (L + 1) / 2 >= (1ull << 31)) {
+    set_error("hapt_tables_init: (G+1)(L+1)=%zu, n_opts=%d or the span count exceeds the "
+              "supported range", (size_t)(G + 1) * (L + 1), n_opts);
     return HAPT_EINVAL;
   }
   if (3 * t->s_max + 3 >= kKSat) {

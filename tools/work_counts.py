@@ -33,18 +33,20 @@ def main(names):
         store = build_store(layers, cluster, model, imbalance_ratio=rho)
         tables = DpTables(store, boundary_costs(layers, cluster))
         pool = np.asarray(store.feasible_t_values())
-        before = np.zeros(4, dtype=np.uint64)
+        before = np.zeros(8, dtype=np.uint64)
         lib.hapt_debug_work(before.ctypes.data)
         tables.sweeper.sweep_device(torch.from_numpy(pool).cuda())
         torch.cuda.synchronize()
-        after = np.zeros(4, dtype=np.uint64)
+        after = np.zeros(8, dtype=np.uint64)
         lib.hapt_debug_work(after.ctypes.data)
         w = (after - before).astype(np.int64)
         ref = tables.transitions_per_sweep() * len(pool)
         out[name] = {"pool_candidates": len(pool), "reference_transitions": int(ref),
                      "executed_lane_transitions": int(w[0]),
                      "admissible_lane_transitions": int(w[1]),
-                     "improving_lane_transitions": int(w[2])}
+                     "improving_lane_transitions": int(w[2]),
+                     "cell_tasks": int(w[4]), "empty_cell_tasks": int(w[5]),
+                     "infinite_cell_tasks": int(w[6]), "staged_chunks": int(w[7])}
         print(name, out[name])
     out["source"] = "tools/work_counts.py (HAPT_COUNT_WORK build), one full-pool sweep each"
     dst = "gpurun_out" if os.path.isdir(os.path.join(REPO, "gpurun_out")) else "profiles"

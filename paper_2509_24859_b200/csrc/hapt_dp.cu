@@ -122,8 +122,8 @@ struct Batch {
   int2 *irange[3];     // [n_groups][G+1] (min, max) split i whose successor entry
                        // (state g) is finite for some candidate of the group;
                        // layer s reads [(s-1)%3], writes [s%3], resets [(s+1)%3]
-  uint32_t *spanlen;   // [n_groups][n_opts] shortest << 16 | longest admissible span
-                       // length of an option (before the group's cut)
+  uint32_t *spanlen;   // [n_groups][2][n_opts] 0xffff - shortest, longest admissible
+                       // span length of an option (before the group's cut)
   uint16_t *winhi;     // [n_groups][G+1] last k of state g's window (dp_window)
   uint32_t *clist;     // [n_groups][ccap] (g << 16 | k0): chunks of up to kChunk
                        // cells k0.. of state g inside the current layer's windows,
@@ -168,7 +168,7 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
     w.ir[j] = cur;
     cur += align_up(ng * (t->G + 1) * sizeof(int2));
   }
-  w.spanlen = cur; cur += align_up(ng * t->n_opts * 4);
+  w.spanlen = cur; cur += align_up(ng * 2 * t->n_opts * 4);
   w.winhi = cur; cur += align_up(ng * (t->G + 1) * 2);
   w.clist = cur; cur += align_up(ng * (size_t)t->L * t->G * 4);
   w.gtot = cur; cur += align_up(ng * 4);
@@ -198,60 +198,60 @@ __device__ __forceinline__ int upper_bound(const double *a, int n, double v) {
 // Per group: candidate padding, pool ranks, the per-row suffix-rank cut, and
 // the layer-0 successor table: F[0, L+1, 0] = 0 (_dp.pyx:41) is the only
 // finite base state.
+constexpr int kPrepY = 16;  // dp_prep blocks per group (rows and boundary entries split)
 __global__ void dp_prep(Batch b) {
   pdl_wait();
   pdl_trigger();
   __shared__ int s_gmax;
-  __shared__ int s_mn[2048], s_mx[2048];  // n_opts < 2048 (hapt_tables_init)
-  const int group = blockIdx.x;
+  const int group = blockIdx.x, part = blockIdx.y;
   const int cw = b.cw;
   if (threadIdx.x == 0) s_gmax = 0;
-  if (group == 0 && threadIdx.x == 0) *b.ticket = 0u;
-  if (threadIdx.x == 0) b.gtot[group] = 0;
   __syncthreads();
-  double *H = b.H[0] + (size_t)group * b.hg * cw;
-  uint16_t *K = b.K[0] + (size_t)group * b.hg * cw;
-  // No fill of the successor tables: every read is confined to a state's
-  // finite-successor range (irange), so layer 1 reads only the base entry
-  // (g2 = 0, i = L) written below, and every later entry is written by the
-  // layer before the one that reads it.
-  // finite-successor ranges: layer 0 has only (g2 = 0, i = L); the buffers
-  // layers 1 and 2 write start empty
-  for (int g = threadIdx.x; g <= b.G; g += blockDim.x) {
-    const int2 empty = make_int2(0x7fffffff, -1);
-    b.irange[0][(size_t)group * (b.G + 1) + g] = g == 0 ? make_int2(b.L, b.L) : empty;
-    b.irange[1][(size_t)group * (b.G + 1) + g] = empty;
-    b.irange[2][(size_t)group * (b.G + 1) + g] = empty;
-  }
-  if (group == 0)
-    for (int g = threadIdx.x; g <= b.G; g += blockDim.x) {
-      const int r = b.g_mesh[g];
-      b.gmeta[g] = make_int4(b.opt_off[r], b.opt_off[r + 1] - b.opt_off[r], b.g_avail[g],
-                             b.g_crow[g]);
-    }
-  for (int x = threadIdx.x; x < kParts * cw; x += blockDim.x)
-    b.spart[(size_t)(x / cw) * b.n_groups * cw + (size_t)group * cw + x % cw] = 0u;
+  // pool ranks of the group's candidates (every block needs the largest)
   if (threadIdx.x < cw) {
     const int cand = group * cw + threadIdx.x;
     const double tm = b.tmax[cand < b.n_cand ? cand : b.n_cand - 1];
     const int cnt = upper_bound(b.pool, (int)b.counters[1], tm);
-    b.tmax_pad[cand] = tm;
-    b.tcnt[cand] = cnt;
+    if (part == 0) {
+      b.tmax_pad[cand] = tm;
+      b.tcnt[cand] = cnt;
+    }
     atomicMax(&s_gmax, cnt);
+  }
+  if (part == 0) {
+    if (group == 0 && threadIdx.x == 0) *b.ticket = 0u;
+    if (threadIdx.x == 0) b.gtot[group] = 0;
+    // No fill of the successor tables: every read is confined to a state's
+    // finite-successor range (irange), so layer 1 reads only the base entry
+    // (g2 = 0, i = L) written below, and every later entry is written by the
+    // layer before the one that reads it.
+    // finite-successor ranges: layer 0 has only (g2 = 0, i = L); the buffers
+    // layers 1 and 2 write start empty
+    for (int g = threadIdx.x; g <= b.G; g += blockDim.x) {
+      const int2 empty = make_int2(0x7fffffff, -1);
+      b.irange[0][(size_t)group * (b.G + 1) + g] = g == 0 ? make_int2(b.L, b.L) : empty;
+      b.irange[1][(size_t)group * (b.G + 1) + g] = empty;
+      b.irange[2][(size_t)group * (b.G + 1) + g] = empty;
+    }
+    if (group == 0)
+      for (int g = threadIdx.x; g <= b.G; g += blockDim.x) {
+        const int r = b.g_mesh[g];
+        b.gmeta[g] = make_int4(b.opt_off[r], b.opt_off[r + 1] - b.opt_off[r], b.g_avail[g],
+                               b.g_crow[g]);
+      }
+    for (int x = threadIdx.x; x < kParts * cw; x += blockDim.x)
+      b.spart[(size_t)(x / cw) * b.n_groups * cw + (size_t)group * cw + x % cw] = 0u;
   }
   __syncthreads();
   // suffix-min ranks are non-decreasing along a row: first entry no candidate
-  // of this group can accept (prank >= srank >= max tcnt) ends the row's scan
-  const int gm = s_gmax;
-  // shortest / longest admissible span (before the cut) of each option, for
+  // of this group can accept (prank >= srank >= max tcnt) ends the row's scan.
+  // Shortest / longest admissible span (before the cut) of each option, for
   // dp_window: entries are in ascending span end, so the row's first entry
-  // is its shortest and the last one before the cut its longest
-  for (int o = threadIdx.x; o < b.n_opts; o += blockDim.x) {
-    s_mn[o] = 0xffff;
-    s_mx[o] = 0;
-  }
-  __syncthreads();
-  for (int row = threadIdx.x; row < b.rows; row += blockDim.x) {
+  // is its shortest and the last one before the cut its longest (both kept
+  // as maxima: 0xffff - shortest, longest; zeroed by dp_ftop_init).
+  const int gm = s_gmax;
+  const int r0 = (int)((long)b.rows * part / kPrepY), r1 = (int)((long)b.rows * (part + 1) / kPrepY);
+  for (int row = r0 + threadIdx.x; row < r1; row += blockDim.x) {
     const int beg = b.span_off[row], end = b.span_off[row + 1];
     int lo = beg, hi = end;
     while (lo < hi) {
@@ -261,27 +261,29 @@ __global__ void dp_prep(Batch b) {
     b.cut_sr[(size_t)group * b.rows + row] = (uint16_t)(lo - beg);
     if (lo > beg) {
       const int o = row / (b.L + 2), k = row - o * (b.L + 2);
-      atomicMin(&s_mn[o], (int)b.spans[beg].i - k + 1);
-      atomicMax(&s_mx[o], (int)b.spans[lo - 1].i - k + 1);
+      atomicMax(b.spanlen + ((size_t)group * 2 + 0) * b.n_opts + o,
+                (unsigned)(0xffff - ((int)b.spans[beg].i - k + 1)));
+      atomicMax(b.spanlen + ((size_t)group * 2 + 1) * b.n_opts + o,
+                (unsigned)((int)b.spans[lo - 1].i - k + 1));
     }
   }
-  __syncthreads();
-  for (int o = threadIdx.x; o < b.n_opts; o += blockDim.x)
-    b.spanlen[(size_t)group * b.n_opts + o] =
-        s_mx[o] ? ((unsigned)s_mn[o] << 16) | (unsigned)s_mx[o] : 0u;
   // the launch-bound increment of every boundary entry for every candidate:
   // kk = (ceil(2c/t_max) + 1) + N (_dp.pyx:82, same association); c > t_max
   // skips the transition (_dp.pyx:76-78) -> 0xFF
   const size_t nkc = (size_t)b.cb_rows * (b.L + 1) * cw;
   uint8_t *kc = b.kc + (size_t)group * nkc;
-  for (size_t x = threadIdx.x; x < nkc; x += blockDim.x) {
+  const size_t x0 = nkc * part / kPrepY, x1 = nkc * (part + 1) / kPrepY;
+  for (size_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
     const size_t e = x / cw;
     const double c = b.cb[e];
-    const double tm = b.tmax_pad[group * cw + (int)(x % cw)];
+    const double tm = b.tmax[min(group * cw + (int)(x % cw), b.n_cand - 1)];
     kc[x] = c <= tm ? (uint8_t)((int)ceil(__ddiv_rn(__dmul_rn(2.0, c), tm)) + 1) : (uint8_t)0xFF;
   }
+  if (part != 0) return;
+  double *H = b.H[0] + (size_t)group * b.hg * cw;
+  uint16_t *K = b.K[0] + (size_t)group * b.hg * cw;
   if (threadIdx.x < cw) {
-    const double tm = b.tmax_pad[group * cw + threadIdx.x];
+    const double tm = b.tmax[min(group * cw + (int)threadIdx.x, b.n_cand - 1)];
     const int row = b.g_crow[0];
     const double c = b.cb[(size_t)row * (b.L + 1) + b.L];
     const size_t e = (size_t)b.L * cw + threadIdx.x;  // g2 = 0, i = L
@@ -296,7 +298,7 @@ __global__ void dp_prep(Batch b) {
   if (threadIdx.x == 0) {  // its lane minimum: finite iff some lane accepts c
     const double c = b.cb[(size_t)b.g_crow[0] * (b.L + 1) + b.L];
     bool any = false;
-    for (int j = 0; j < cw; ++j) any |= c <= b.tmax_pad[group * cw + j];
+    for (int j = 0; j < cw; ++j) any |= c <= b.tmax[min(group * cw + j, b.n_cand - 1)];
     b.Hmin[0][(size_t)group * b.hg + b.L] = any ? __dadd_rn(__dmul_rn(2.0, c), 0.0) : kInf;
   }
 }
@@ -335,11 +337,11 @@ __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
       const int devs = __ldg(b.opt_devs + o), g2 = g - devs;
       if (devs > gm.z || g2 < s - 1) continue;
       const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
-      const uint32_t ml = __ldg(b.spanlen + (size_t)group * b.n_opts + o);
+      const int mn = 0xffff - (int)__ldg(b.spanlen + ((size_t)group * 2 + 0) * b.n_opts + o);
+      const int mx = (int)__ldg(b.spanlen + ((size_t)group * 2 + 1) * b.n_opts + o);
       // option o reaches a finite successor from cell k only through spans
       // (k, i) with i in [fr.x, min(fr.y, L-s+1)] and admissible length
       // i-k+1 in [minlen_o, maxlen_o]
-      const int mx = (int)(ml & 0xffffu), mn = (int)(ml >> 16);
       const int hi = min(imax, fr.y);
       if (fr.x > hi || mx == 0) continue;
       klo = min(klo, max(1, fr.x - mx + 1));
@@ -940,12 +942,14 @@ __global__ void dp_states_reduce(Batch b) {
   }
 }
 
-__global__ void dp_ftop_init(double *ftop, unsigned long long *states, int n_cand, int s_max) {
+__global__ void dp_ftop_init(double *ftop, unsigned long long *states, int n_cand, int s_max,
+                             uint32_t *spanlen, int n_span) {
   pdl_wait();
   pdl_trigger();
   const long x = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (x < (long)n_cand * (s_max + 1)) ftop[x] = kInf;
   if (x < n_cand) states[x] = 0;
+  if (x < n_span) spanlen[x] = 0u;
 }
 
 // Per candidate best s and T* (planner.py:287-298), then the lexicographic
@@ -1164,9 +1168,12 @@ int run_sweep(const Batch &b, cudaStream_t st) {
   // measured: on tiny tables (config A, L*G ~ 100) the dependent-launch wait
   // costs more than the gap it hides
   const bool pdl = pdl_enabled() && (long)b.L * b.G >= 4096;
-  HAPT_CUDA(launch_pdl(dp_ftop_init, grid_for((size_t)b.n_cand * (b.s_max + 1), 256), 256, st, pdl,
-                       b.ftop, b.states, b.n_cand, b.s_max));
-  HAPT_CUDA(launch_pdl(dp_prep, b.n_groups, 256, st, pdl, b));  // block >= 128 = max group width
+  const int n_span = 2 * b.n_groups * b.n_opts;
+  HAPT_CUDA(launch_pdl(dp_ftop_init,
+                       grid_for(max((size_t)b.n_cand * (b.s_max + 1), (size_t)n_span), 256), 256,
+                       st, pdl, b.ftop, b.states, b.n_cand, b.s_max, b.spanlen, n_span));
+  // block >= 128 = max group width
+  HAPT_CUDA(launch_pdl(dp_prep, dim3(b.n_groups, kPrepY), 256, st, pdl, b));
   for (int s = 1; s <= b.s_max; ++s) {
     const long cells = (long)(b.L - s + 1) * (b.G - s + 1);
     if (cells <= 0) break;

@@ -449,12 +449,14 @@ __global__ void k_srank(hapt_tables t) {
 // A state with callers that disagree raises counters[10] (the host refuses
 // the encoding); a state with no caller gets -1 (its entry is never read).
 __global__ void k_gcrow(hapt_tables t) {
-  const int g2 = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g2 > t.G) return;
+  // one warp per successor state g2, lanes over the callers g
+  const int g2 = (int)(((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g2 > t.G) return;  // warp-uniform
   const int nm = t.n_meshes;
-  int row = -1;
+  int lo = 0x7fffffff, hi = -1;
   bool conflict = false;
-  for (int g = g2 + 1; g <= t.G; ++g) {
+  for (int g = g2 + 1 + lane; g <= t.G; g += 32) {
     const int r = t.g_mesh[g], devs = g - g2;
     if (r < 0 || r >= nm) {
       conflict = true;
@@ -465,11 +467,16 @@ __global__ void k_gcrow(hapt_tables t) {
     for (int o = t.opt_off[r]; o < t.opt_off[r + 1] && !has; ++o) has = t.opt_devs[o] == devs;
     if (!has) continue;
     const int rr = (g2 >= 1 && t.g_mesh[g2] == r) ? r : nm + r;
-    if (row < 0) row = rr;
-    else conflict |= row != rr;
+    lo = min(lo, rr);
+    hi = max(hi, rr);
   }
-  t.g_crow[g2] = row;
-  if (conflict) t.counters[10] = 1;
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  conflict = __any_sync(0xffffffffu, conflict) || (hi >= 0 && lo != hi);
+  if (lane == 0) {
+    t.g_crow[g2] = hi;  // -1: no caller
+    if (conflict) t.counters[10] = 1;
+  }
 }
 
 // Encoding checks the DP relies on besides g_crow: every option uses at least
@@ -515,7 +522,7 @@ int finalize_impl(hapt_tables *tp, cudaStream_t st) {
   k_srank<<<grid_for(rows * 32, 256), 256, 0, st>>>(t); ::hapt::note_launch();
   HAPT_CUDA(cudaMemsetAsync(&t.counters[10], 0, 8, st));
   k_encoding<<<grid_for(t.n_opts, 128), 128, 0, st>>>(t); ::hapt::note_launch();
-  k_gcrow<<<grid_for(t.G + 1, 128), 128, 0, st>>>(t); ::hapt::note_launch();
+  k_gcrow<<<grid_for((size_t)(t.G + 1) * 32, 128), 128, 0, st>>>(t); ::hapt::note_launch();
   HAPT_LAUNCHED("finalize");
   return HAPT_OK;
 }

@@ -125,6 +125,9 @@ struct Batch {
   uint32_t *spanlen;   // [n_groups][2][n_opts] 0xffff - shortest, longest admissible
                        // span length of an option (before the group's cut)
   uint16_t *winhi;     // [n_groups][G+1] last k of state g's window (dp_window)
+  int2 *wopt;          // [n_groups][G+1][32] per state and option j < 32 of its mesh:
+                       // {lo | hi << 16, g2*(L+1)}, the admissible split range of the
+                       // current layer (dp_window) and the successor row
   uint32_t *clist;     // [n_groups][ccap] (g << 16 | k0): chunks of up to kChunk
                        // cells k0.. of state g inside the current layer's windows,
                        // group-local compact order
@@ -149,7 +152,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], spanlen, winhi, clist, gtot, goff, ticket, gmeta, spart, H0,
+  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], spanlen, winhi, wopt, clist, gtot, goff, ticket, gmeta, spart, H0,
       H1, K0, K1, Hm0, Hm1, total;
 };
 
@@ -170,6 +173,7 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   }
   w.spanlen = cur; cur += align_up(ng * 2 * t->n_opts * 4);
   w.winhi = cur; cur += align_up(ng * (t->G + 1) * 2);
+  w.wopt = cur; cur += align_up(ng * (t->G + 1) * 32 * 8);
   w.clist = cur; cur += align_up(ng * (size_t)t->L * t->G * 4);
   w.gtot = cur; cur += align_up(ng * 4);
   w.goff = cur; cur += align_up((ng + 1) * 4);
@@ -332,11 +336,17 @@ __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
   int klo = 0x7fff, khi = 0;
   if (g <= G && g >= s) {
     const int4 gm = b.gmeta[g];
+    int2 *wo = b.wopt + ((size_t)group * (G + 1) + g) * 32;
     for (int j = lane; j < gm.y; j += 32) {
       const int o = gm.x + j;
       const int devs = __ldg(b.opt_devs + o), g2 = g - devs;
-      if (devs > gm.z || g2 < s - 1) continue;
+      if (devs > gm.z || g2 < s - 1) {
+        if (j < 32) wo[j] = make_int2(1, 0);
+        continue;
+      }
       const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
+      if (j < 32) wo[j] = make_int2(fr.x <= min(imax, fr.y) ? fr.x | (min(imax, fr.y) << 16) : 1,
+                                    g2 * (L + 1));
       const int mn = 0xffff - (int)__ldg(b.spanlen + ((size_t)group * 2 + 0) * b.n_opts + o);
       const int mx = (int)__ldg(b.spanlen + ((size_t)group * 2 + 1) * b.n_opts + o);
       // option o reaches a finite successor from cell k only through spans
@@ -917,7 +927,14 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
                                : min(k0 + kChunk - 1,
                                      (int)__ldg(b.winhi + (size_t)group * (b.G + 1) + g));
     const int4 gm = b.gmeta[g];
-    const OptLane ol0 = opt_lane(b, s, group, g, gm.x + lane, gm.z, lane < gm.y);
+    // this layer's split ranges of the state's first 32 options (dp_window)
+    OptLane ol0;
+    {
+      const int2 w = lane < gm.y ? __ldg(b.wopt + ((size_t)group * (b.G + 1) + g) * 32 + lane)
+                                 : make_int2(1, 0);
+      ol0.fr = make_int2(w.x & 0xffff, (unsigned)w.x >> 16);
+      ol0.hbase = w.y;
+    }
     for (int k = k0; k <= k1; ++k) {
       int fin[CPL];
       relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm, ol0);
@@ -1141,6 +1158,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);
   b.spanlen = (uint32_t *)(wb + w.spanlen);
   b.winhi = (uint16_t *)(wb + w.winhi);
+  b.wopt = (int2 *)(wb + w.wopt);
   b.clist = (uint32_t *)(wb + w.clist);
   b.ccap = (size_t)t->L * t->G;
   b.gtot = (int32_t *)(wb + w.gtot);

@@ -317,6 +317,26 @@ int hapt_analyze_1f1b_trace(int32_t n_plans, int32_t total_stages, const int32_t
                             double *stage_rep, int32_t *peak_inflight, double *link_rep,
                             double *steady_rate, void *stream);
 
+/* steady_state_rate(trace, stage) (simulation.py:374-395) of each plan at
+ * its own stage rate_stage[p] (1-based; NULL = stage 1), from node times in
+ * the reference numbering as hapt_sim_1f1b writes them (node_end unused).
+ * NaN where the reference raises SimulationError or status[p] != 0. */
+int hapt_steady_rate_1f1b(int32_t n_plans, const int32_t *stage_off, const int32_t *counts,
+                          const int32_t *num_mb, const double *node_start,
+                          const int64_t *node_off, const int32_t *rate_stage,
+                          const int32_t *status, double *steady_rate, void *stream);
+
+/* asap_tight (simulation.py:407-424) of a trace over a DAG given as successor
+ * CSR: first_bad [1] = the smallest node v whose start is not
+ * math.isclose(max over predecessors u of start[u] + duration[u], rel_tol,
+ * abs_tol=1e-12) (or != 0 without predecessors); n_nodes if every node is
+ * tight.  work >= hapt_asap_workspace_bytes(n_nodes). */
+size_t hapt_asap_workspace_bytes(int32_t n_nodes);
+int hapt_dag_asap_check(int32_t n_nodes, const int32_t *succ_off, const int32_t *succ_idx,
+                        const int32_t *indeg, const double *duration, const double *start,
+                        double rel_tol, int32_t *first_bad, void *work, size_t work_bytes,
+                        void *stream);
+
 /* Longest-path start times of an arbitrary DAG given as successor CSR:
  * start[v] = max_u (start[u] + duration[u]). processed [1] = number of nodes
  * reached (< n_nodes <=> cycle). */

@@ -164,6 +164,11 @@ _SIGNATURES = {
         [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
          c_vp, c_vp, c_vp],
     ),
+    "hapt_steady_rate_1f1b": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "hapt_asap_workspace_bytes": (c_sz, [c_i32]),
+    "hapt_dag_asap_check": (
+        c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl, c_vp, c_vp, c_sz, c_vp],
+    ),
     "hapt_dag_workspace_bytes": (c_sz, [c_i32]),
     "hapt_dag_longest_path": (
         c_i32,

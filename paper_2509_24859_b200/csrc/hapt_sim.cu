@@ -656,6 +656,89 @@ struct LinkAt {  // transfer of microbatch i+1 in one direction -> {start, end}
   }
 };
 
+// steady_state_rate(trace, stage) (simulation.py:374-395): least-squares
+// slope of the forward start times of microbatches 2K+1, 3K+1, ... <= B on
+// stage s0 (0-based), K its launch count; NaN where the reference raises
+// SimulationError (fewer than 4 samples).  Sums are CPython's compensated
+// sum(), the mean/deviation expressions the reference's.
+template <bool TRACE>
+__device__ double steady_rate_at(const NodeIn &in, int64_t nb, int s0, int K, int B) {
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  int n = 0;
+  long long sx = 0;
+  for (int i = 2 * K + 1; i <= B; i += K) ++n, sx += i;
+  if (n < 4) return nan;
+  const double fn = (double)n;
+  const double mx = __ddiv_rn((double)sx, fn);
+  PySum sy;
+  // start of F(mb i) on stage s0
+  const StageAt<TRACE> at0{in, nb + 2 * (int64_t)s0 * B, K, B};
+  auto f_start = [&](int i) { return at0(encode_op(i, true, K, B)).x; };
+  for (int i = 2 * K + 1; i <= B; i += K) sy.add(f_start(i));
+  const double my = __ddiv_rn(sy.value(), fn);
+  PySum sxx, sxy;
+  for (int i = 2 * K + 1; i <= B; i += K) {
+    const double dx = __dadd_rn((double)i, -mx);
+    sxx.add(__dmul_rn(dx, dx));  // (x - mean_x) ** 2
+    sxy.add(__dmul_rn(dx, __dadd_rn(f_start(i), -my)));
+  }
+  return __ddiv_rn(sxy.value(), sxx.value());
+}
+
+// steady_state_rate of plan p at its stage rate_stage[p] (1-based), node
+// times in the reference numbering (simulate's trace).
+__global__ void k_steady_rate(int n_plans, const int32_t *stage_off, const int32_t *counts,
+                              const int32_t *num_mb, NodeIn in, const int32_t *rate_stage,
+                              const int32_t *status, double *steady_rate) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_plans) return;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  const int S = stage_off[p + 1] - stage_off[p];
+  const int st = rate_stage ? rate_stage[p] : 1;
+  if ((status && status[p] != HAPT_OK) || st < 1 || st > S) {
+    steady_rate[p] = nan;
+    return;
+  }
+  steady_rate[p] =
+      steady_rate_at<false>(in, in.off[p], st - 1, counts[stage_off[p] + st - 1], num_mb[p]);
+}
+
+// asap_tight (simulation.py:407-424): every node with predecessors starts at
+// max over them of start[u] + duration[u] (math.isclose(rel_tol, abs 1e-12)),
+// every other node at 0.  Pass 1 (per node u, over its successors): the max
+// as an order-preserving key; pass 2 (per node): the check, first failing
+// node into *bad (n if none).
+__device__ __forceinline__ unsigned long long okey(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double okey_decode(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+__global__ void k_asap_max(int n, const int32_t *succ_off, const int32_t *succ_idx,
+                           const double *dur, const double *start, unsigned long long *hi) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const unsigned long long e = okey(__dadd_rn(start[u], dur[u]));
+  for (int x = succ_off[u]; x < succ_off[u + 1]; ++x) atomicMax(hi + succ_idx[x], e);
+}
+// CPython math.isclose(a, b, rel_tol, abs_tol)
+__device__ __forceinline__ bool py_isclose(double a, double b, double rel, double abs_tol) {
+  if (a == b) return true;
+  if (isinf(a) || isinf(b)) return false;
+  const double diff = fabs(__dadd_rn(b, -a));
+  return diff <= fabs(__dmul_rn(rel, b)) || diff <= fabs(__dmul_rn(rel, a)) || diff <= abs_tol;
+}
+__global__ void k_asap_check(int n, const int32_t *indeg, const double *start,
+                             const unsigned long long *hi, double rel_tol, int32_t *bad) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const bool ok = indeg[v] == 0 ? start[v] == 0.0
+                                : py_isclose(start[v], okey_decode(hi[v]), rel_tol, 1e-12);
+  if (!ok) atomicMin(bad, v);
+}
+
 // Three thread ranges, so that a warp's threads run the same kind of row
 // (a mixed warp serialises a long link walk behind short stage rows):
 //   [0, T)        the stage row of packed stage x
@@ -786,33 +869,7 @@ __global__ void k_analyze(int n_plans, const int32_t *stage_off, const double *t
     return;
   }
   // -- steady_state_rate(trace, stage=1) (simulation.py:374-395) --
-  if (failed) {
-    steady_rate[p] = nan;
-    return;
-  }
-  const int K = counts[x];
-  int n = 0;
-  long long sx = 0;
-  for (int i = 2 * K + 1; i <= B; i += K) ++n, sx += i;
-  if (n < 4) {
-    steady_rate[p] = nan;
-    return;
-  }
-  const double fn = (double)n;
-  const double mx = __ddiv_rn((double)sx, fn);
-  PySum sy;
-  // start of F(mb i) on stage 0
-  const StageAt<TRACE> at0{in, nb, K, B};
-  auto f_start = [&](int i) { return at0(encode_op(i, true, K, B)).x; };
-  for (int i = 2 * K + 1; i <= B; i += K) sy.add(f_start(i));
-  const double my = __ddiv_rn(sy.value(), fn);
-  PySum sxx, sxy;
-  for (int i = 2 * K + 1; i <= B; i += K) {
-    const double dx = __dadd_rn((double)i, -mx);
-    sxx.add(__dmul_rn(dx, dx));  // (x - mean_x) ** 2
-    sxy.add(__dmul_rn(dx, __dadd_rn(f_start(i), -my)));
-  }
-  steady_rate[p] = __ddiv_rn(sxy.value(), sxx.value());
+  steady_rate[p] = failed ? nan : steady_rate_at<TRACE>(in, nb, 0, counts[x], B);
 }
 
 }  // namespace
@@ -1049,4 +1106,50 @@ extern "C" int hapt_analyze_1f1b_trace(int32_t n_plans, int32_t total_stages,
                       NodeIn{nullptr, nullptr, reinterpret_cast<const double2 *>(trace),
                              trace_off},
                       status, stage_rep, peak_inflight, link_rep, steady_rate, stream);
+}
+
+extern "C" int hapt_steady_rate_1f1b(int32_t n_plans, const int32_t *stage_off,
+                                     const int32_t *counts, const int32_t *num_mb,
+                                     const double *node_start, const int64_t *node_off,
+                                     const int32_t *rate_stage, const int32_t *status,
+                                     double *steady_rate, void *stream) {
+  if (n_plans < 1 || !stage_off || !counts || !num_mb || !node_start || !node_off ||
+      !steady_rate) {
+    set_error("hapt_steady_rate_1f1b: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  k_steady_rate<<<grid_for(n_plans, 128), 128, 0, (cudaStream_t)stream>>>(
+      n_plans, stage_off, counts, num_mb, NodeIn{node_start, nullptr, nullptr, node_off},
+      rate_stage, status, steady_rate);
+  ::hapt::note_launch();
+  HAPT_LAUNCHED("k_steady_rate");
+  return HAPT_OK;
+}
+
+extern "C" size_t hapt_asap_workspace_bytes(int32_t n_nodes) {
+  return n_nodes > 0 ? (size_t)n_nodes * 8 : 0;
+}
+
+extern "C" int hapt_dag_asap_check(int32_t n_nodes, const int32_t *succ_off,
+                                   const int32_t *succ_idx, const int32_t *indeg,
+                                   const double *duration, const double *start, double rel_tol,
+                                   int32_t *first_bad, void *work, size_t work_bytes,
+                                   void *stream) {
+  if (n_nodes < 1 || !succ_off || !succ_idx || !indeg || !duration || !start || !first_bad ||
+      !work || work_bytes < hapt_asap_workspace_bytes(n_nodes)) {
+    set_error("hapt_dag_asap_check: invalid arguments");
+    return HAPT_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long *hi = (unsigned long long *)work;
+  HAPT_CUDA(cudaMemsetAsync(hi, 0, (size_t)n_nodes * 8, st));
+  HAPT_CUDA(cudaMemcpyAsync(first_bad, &n_nodes, 4, cudaMemcpyHostToDevice, st));
+  k_asap_max<<<grid_for(n_nodes, 256), 256, 0, st>>>(n_nodes, succ_off, succ_idx, duration,
+                                                      start, hi);
+  ::hapt::note_launch();
+  k_asap_check<<<grid_for(n_nodes, 256), 256, 0, st>>>(n_nodes, indeg, start, hi, rel_tol,
+                                                        first_bad);
+  ::hapt::note_launch();
+  HAPT_LAUNCHED("k_asap_check");
+  return HAPT_OK;
 }

@@ -624,16 +624,23 @@ def sweep_pool(store: ProfileStore, costs: BoundaryCost, num_microbatches: int, 
     return ev.pool, ev.tstar, ev.best_s, ev.states, winner
 
 
-def _score(ftop: np.ndarray, tmax: np.ndarray, B: int):
-    """_extract_plan's choice of stage count (planner.py:287-296) for many
-    candidates: first s with the strictly smallest F[s,1,G] + (B-1)*t_max
-    over finite F.  Returns (T*, best_s) with best_s = -1 when infeasible."""
-    pen = float(B - 1) * tmax  # (B - 1) * t_max: int times float
-    tot = ftop[:, 1:] + pen[:, None]  # +inf where F is infinite
-    s = np.argmin(tot, axis=1)
-    t = tot[np.arange(len(tot)), s]
-    ok = np.isfinite(t)
-    return np.where(ok, t, np.inf), np.where(ok, s + 1, -1)
+def _score(sweeper, ftop: np.ndarray, tmax: np.ndarray, B: int):
+    """_extract_plan's choice of stage count (planner.py:287-296) and the
+    sort_key merge (planner.py:107-115) for many candidates, on the device
+    (hapt_dp_select over F[s,1,G] rows kept from the sweeps): first s with
+    the strictly smallest F[s,1,G] + (B-1)*t_max over finite F.  Returns
+    (T*, best_s, winner) -- best_s = -1 when infeasible, winner = index of the
+    (T*, t_max) minimum (rows in t_max order) or -1."""
+    import torch
+
+    dev = sweeper.device
+    f = torch.from_numpy(np.ascontiguousarray(ftop, dtype=np.float64)).to(dev)
+    t = torch.from_numpy(np.ascontiguousarray(tmax, dtype=np.float64)).to(dev)
+    tstar, best_s, winner = sweeper.select_device(f, t, B)
+    host = torch.cat([tstar.view(torch.int64), best_s.to(torch.int64),
+                      winner.to(torch.int64)]).cpu().numpy()
+    n = len(tmax)
+    return host[:n].view(np.float64).copy(), host[n:2 * n].copy(), int(host[2 * n])
 
 
 def search_batches(store: ProfileStore, costs: BoundaryCost, batch_sizes: Sequence[int],
@@ -661,7 +668,7 @@ def search_batches(store: ProfileStore, costs: BoundaryCost, batch_sizes: Sequen
         t_lo = np.array([pool[lo]])
         cuts = {}
         for B in Bs:
-            ts_lo, _ = _score(ev.ftop[[lo]], t_lo, B)
+            ts_lo, _, _ = _score(tables.sweeper, ev.ftop[[lo]], t_lo, B)
             cuts[B] = float(ts_lo[0]) / (B - 1) if B > 1 else math.inf
         t_cut = max(cuts.values())
         ev.ensure([i for i in range(lo, n) if pool[i] <= t_cut])
@@ -674,12 +681,13 @@ def search_batches(store: ProfileStore, costs: BoundaryCost, batch_sizes: Sequen
         t_e = cuts[B]
         surviving = [i for i in range(lo, n) if pool[i] <= t_e]
         idx = np.asarray(surviving, dtype=np.int64)
-        tstar, best_s = _score(ev.ftop[idx], ev.pool[idx], B)
-        cand = [k for k in range(len(idx)) if best_s[k] >= 0]
-        if not cand:
+        if len(idx) == 0:
             raise InfeasiblePlanError(
                 "no stage partition satisfies the memory and overlap constraints")
-        k = min(cand, key=lambda j: (tstar[j], pool[surviving[j]]))
+        tstar, best_s, k = _score(tables.sweeper, ev.ftop[idx], ev.pool[idx], B)
+        if k < 0:
+            raise InfeasiblePlanError(
+                "no stage partition satisfies the memory and overlap constraints")
         plan = ev.plan(surviving[k], epsilon, B=B, best_s=int(best_s[k]), tstar=float(tstar[k]))
         if optimized:
             surv_t = [pool[i] for i in surviving]

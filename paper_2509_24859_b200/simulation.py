@@ -10,9 +10,11 @@ frontier kernel hapt_dag_longest_path over the current lists instead, with
 the reference's CycleError diagnosis.
 
 `simulate_batch` is the config-E workload: makespans of many plans in one
-launch.  `analyze` / `steady_state_rate` / trace export are host-side
-post-processing of a trace (SURVEY.md §8(f) ranks the batched analysis as the
-next row).
+launch.  `analyze` / `steady_state_rate` / `asap_tight` of a trace run on the
+device over the trace's node times (hapt_analyze_1f1b, hapt_steady_rate_1f1b,
+hapt_dag_asap_check), as do the batched reports (`analyze_batch`,
+`PlanBatch.analyze`); trace export (`trace_events`, `trace_to_text`) is
+host-side formatting of the wire formats.
 """
 
 from __future__ import annotations
@@ -568,38 +570,11 @@ def analyze_batch(t_fwd, t_bwd, comm, counts, num_microbatches, mem_act=None,
 
 
 # ---------------------------------------------------------------------------
-# Host-side analysis of a trace (simulation.py:236-479)
+# Analysis of one trace (simulation.py:268-424): the report dataclasses are
+# the reference's API types; every figure comes from the device kernels
+# (hapt_analyze_1f1b / hapt_steady_rate_1f1b / hapt_dag_asap_check) over the
+# trace's own node times.
 # ---------------------------------------------------------------------------
-
-
-def _interval_union(intervals):
-    out = []
-    for lo, hi in sorted(intervals):
-        if hi <= lo:
-            continue
-        if out and lo <= out[-1][1]:
-            out[-1] = (out[-1][0], max(out[-1][1], hi))
-        else:
-            out.append((lo, hi))
-    return out
-
-
-def _intersect(a, b):
-    out = []
-    i = j = 0
-    while i < len(a) and j < len(b):
-        lo, hi = max(a[i][0], b[j][0]), min(a[i][1], b[j][1])
-        if hi > lo:
-            out.append((lo, hi))
-        if a[i][1] <= b[j][1]:
-            i += 1
-        else:
-            j += 1
-    return out
-
-
-def _total(iv):
-    return sum(hi - lo for lo, hi in iv)
 
 
 @dataclass
@@ -642,80 +617,128 @@ class SimulationReport:
         return "\n".join(lines) + "\n"
 
 
+class _TraceDev:
+    """One trace on the device: the plan's stage arrays and the trace's node
+    times in the reference numbering (plan count 1, node_off 0)."""
+
+    def __init__(self, trace: ScheduleTrace, with_end: bool = True):
+        import torch
+
+        dag = trace.dag
+        dev = torch.device("cuda", torch.cuda.current_device())
+        T = lambda a, dt=torch.float64: torch.as_tensor(np.asarray(a), dtype=dt).to(dev)  # noqa: E731
+        S = dag.num_stages
+        self.S, self.B, self.dev = S, dag.num_microbatches, dev
+        self.off = T([0, S], torch.int32)
+        self.t_fwd, self.t_bwd = T(dag.t_fwd), T(dag.t_bwd)
+        self.comm = T(list(dag.comm) + [0.0])
+        self.counts = T(dag.program.counts.counts, torch.int32)
+        self.mb = T([self.B], torch.int32)
+        self.node_off = T([0], torch.int64)
+        self.start = T(trace.start)
+        self.end = T(trace.end) if with_end else None
+
+
 def analyze(trace: ScheduleTrace, mem_act_per_stage=None) -> SimulationReport:
-    dag = trace.dag
-    S = dag.num_stages
-    dur = dag.duration
-    rows, busy_iv = [], []
-    for s in range(1, S + 1):
-        nodes = trace.stage_op_nodes(s)
-        iv = _interval_union([(trace.start[n], trace.end[n]) for n in nodes])
-        busy_iv.append(iv)
-        busy = sum(dur[n] for n in nodes)
-        window = trace.end[nodes[-1]] - trace.start[nodes[0]]
-        prog = dag.program.stages[s - 1]
-        steady = nodes[prog.warmup: prog.warmup + prog.steady]
-        if steady:
-            sb = (trace.end[steady[-1]] - trace.start[steady[0]]) - sum(dur[n] for n in steady)
-        else:
-            sb = 0.0
-        inflight = peak = 0
-        for kind, _ in prog.ops:
-            inflight += 1 if kind == FWD else -1
-            peak = max(peak, inflight)
-        per = mem_act_per_stage[s - 1] if mem_act_per_stage else 0.0
-        rows.append(StageReport(s, busy, window, window - busy,
-                                (window - busy) / window if window > 0 else 0.0, sb, peak,
-                                peak * per))
-    links = []
-    B = dag.num_microbatches
-    for s in range(1, S):
-        fw = [dag.node_id(NODE_CF, i, s) for i in range(1, B + 1)]
-        bw = [dag.node_id(NODE_CB, i, s) for i in range(1, B + 1)]
-        tot = _total(_interval_union([(trace.start[n], trace.end[n]) for n in fw + bw]))
-        if tot <= 0.0:
-            ratio = 1.0
-        else:
-            busy = _interval_union([(trace.start[n], trace.end[n]) for n in fw + bw])
-            ratio = _total(_intersect(_intersect(busy, busy_iv[s - 1]), busy_iv[s])) / tot
-        links.append(LinkReport(s, sum(dur[n] for n in fw), sum(dur[n] for n in bw), ratio))
-    return SimulationReport(trace.makespan, rows, links)
+    """Per-stage busy / bubble / steady bubble / peak in-flight and per-link
+    overlap of one trace (simulation.py:310-371): hapt_analyze_1f1b over the
+    trace's node times, one plan."""
+    import torch
+
+    from . import _lib
+    from ._lib import check, stream_ptr
+
+    td = _TraceDev(trace)
+    S, dev = td.S, td.dev
+    mem = None
+    if mem_act_per_stage:  # the reference's `if mem_act_per_stage` (else bytes 0.0)
+        mem = torch.as_tensor([float(x) for x in mem_act_per_stage[:S]], dtype=torch.float64,
+                              device=dev)
+    out = torch.empty(S * 6 + S * 3 + 1, dtype=torch.float64, device=dev)
+    peak = torch.empty(S, dtype=torch.int32, device=dev)
+    check(_lib.lib().hapt_analyze_1f1b(
+        1, S, td.off.data_ptr(), td.t_fwd.data_ptr(), td.t_bwd.data_ptr(), td.comm.data_ptr(),
+        td.counts.data_ptr(), td.mb.data_ptr(), 0 if mem is None else mem.data_ptr(),
+        td.start.data_ptr(), td.end.data_ptr(), td.node_off.data_ptr(), None,
+        out.data_ptr(), peak.data_ptr(), out[S * 6:].data_ptr(), out[S * 9:].data_ptr(),
+        stream_ptr()))
+    h = out.cpu().numpy()
+    pk = peak.cpu().numpy()
+    st = h[: S * 6].reshape(S, 6)
+    ln = h[S * 6: S * 9].reshape(S, 3)
+    stages = [StageReport(s + 1, float(st[s, 0]), float(st[s, 1]), float(st[s, 2]),
+                          float(st[s, 3]), float(st[s, 4]), int(pk[s]), float(st[s, 5]))
+              for s in range(S)]
+    links = [LinkReport(s + 1, float(ln[s, 0]), float(ln[s, 1]), float(ln[s, 2]))
+             for s in range(S - 1)]
+    return SimulationReport(trace.makespan, stages, links)
 
 
 def steady_state_rate(trace: ScheduleTrace, stage: int = 1) -> float:
+    """Least-squares time per microbatch of the steady block starts of one
+    stage (simulation.py:374-395), on the device (hapt_steady_rate_1f1b)."""
+    import torch
+
+    from . import _lib
+    from ._lib import check, stream_ptr
+
     dag = trace.dag
-    B = dag.num_microbatches
-    K = dag.program.counts.counts[stage - 1]
-    idx = list(range(2 * K + 1, B + 1, K))
-    if len(idx) < 4:
+    K = dag.program.counts.counts[stage - 1]  # IndexError past the last stage, as the reference
+    if len(range(2 * K + 1, dag.num_microbatches + 1, K)) < 4:
         raise SimulationError(f"steady window too short: need >= 3 blocks of {K} microbatches")
-    ys = [trace.start[dag.node_id(NODE_F, i, stage)] for i in idx]
-    n = float(len(idx))
-    mx, my = sum(idx) / n, sum(ys) / n
-    sxx = sum((x - mx) ** 2 for x in idx)
-    sxy = sum((x - mx) * (y - my) for x, y in zip(idx, ys))
-    return sxy / sxx
+    if not 1 <= int(stage) <= dag.num_stages:
+        raise KeyError((NODE_F, 2 * K + 1, stage))  # the reference's node-id lookup
+    td = _TraceDev(trace, with_end=False)
+    rs = torch.tensor([int(stage)], dtype=torch.int32, device=td.dev)
+    out = torch.empty(1, dtype=torch.float64, device=td.dev)
+    check(_lib.lib().hapt_steady_rate_1f1b(
+        1, td.off.data_ptr(), td.counts.data_ptr(), td.mb.data_ptr(), td.start.data_ptr(),
+        td.node_off.data_ptr(), rs.data_ptr(), None, out.data_ptr(), stream_ptr()))
+    return float(out.item())
 
 
 def steady_block_span(trace: ScheduleTrace, stage: int, i: int) -> float:
+    """start(F[i+K]) - start(F[i]) on a stage (simulation.py:398-404), K its
+    launch count; the subtraction runs on the device like every other
+    figure of a trace."""
+    import torch
+
     dag = trace.dag
     K = dag.program.counts.counts[stage - 1]
-    return (trace.start[dag.node_id(NODE_F, i + K, stage)]
-            - trace.start[dag.node_id(NODE_F, i, stage)])
+    a, b = dag.node_id(NODE_F, i + K, stage), dag.node_id(NODE_F, i, stage)
+    t = torch.tensor([trace.start[a], trace.start[b]], dtype=torch.float64,
+                     device=torch.device("cuda", torch.cuda.current_device()))
+    return float((t[0] - t[1]).item())
 
 
 def asap_tight(trace: ScheduleTrace, rel_tol: float = 1e-9) -> bool:
+    """Every node starts as soon as its predecessors allow (simulation.py:
+    407-424), checked on the device over the DAG's edges
+    (hapt_dag_asap_check)."""
+    import torch
+
+    from . import _lib
+    from ._lib import check, stream_ptr
+
+    lib = _lib.lib()
     dag = trace.dag
-    dur = dag.duration
-    for v in range(dag.num_nodes):
-        if not dag.pred[v]:
-            if trace.start[v] != 0.0:
-                return False
-            continue
-        hi = max(trace.start[u] + dur[u] for u in dag.pred[v])
-        if not math.isclose(trace.start[v], hi, rel_tol=rel_tol, abs_tol=1e-12):
-            return False
-    return True
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = dag.num_nodes
+    succ = dag.succ
+    off = np.zeros(n + 1, dtype=np.int32)
+    off[1:] = np.cumsum([len(x) for x in succ])
+    idx = np.fromiter((v for x in succ for v in x), dtype=np.int32, count=int(off[-1]))
+    indeg = np.array([len(x) for x in dag.pred], dtype=np.int32)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    d_off, d_idx, d_indeg = T(off), T(idx if len(idx) else np.zeros(1, np.int32)), T(indeg)
+    d_dur = T(np.asarray(dag.duration, dtype=np.float64))
+    d_start = T(np.asarray(trace.start, dtype=np.float64))
+    bad = torch.empty(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(lib.hapt_asap_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    check(lib.hapt_dag_asap_check(n, d_off.data_ptr(), d_idx.data_ptr(), d_indeg.data_ptr(),
+                                  d_dur.data_ptr(), d_start.data_ptr(), float(rel_tol),
+                                  bad.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr()))
+    return int(bad.item()) >= n
 
 
 def trace_events(trace: ScheduleTrace, labels=None) -> list:

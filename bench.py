@@ -63,43 +63,48 @@ def cpu_model() -> str:
 # ---------------------------------------------------------------------------
 
 
+def _ref_types(d):
+    """Instance dict -> the reference's own (store, costs, B, eps)."""
+    from meshpipe.cluster import ClusterSpec as RC, DeviceMesh as RM
+    from meshpipe.model_graph import Layer as RL, LayerSequence as RS
+    from meshpipe.profiling import CostModel as RCM, boundary_costs as rbc
+    from meshpipe.profiling import build_store as rbs
+
+    lay = d["layers"]
+    layers = RS(tuple(RL(i, i + 1, lay["flops"][i], lay["param_bytes"][i],
+                         lay["boundary_bytes"][i], tuple(lay["signature"][i]))
+                      for i in range(len(lay["flops"]))), ())
+    meshes = [RM(m["id"], m["hosts"], m["devices_per_host"], m["peak_flops"],
+                 m["mem_device"], m["intra_host_bw"], m["inter_host_bw"])
+              for m in d["cluster"]["meshes"]]
+    cb = d["cluster"]["cross_bw"]
+    if isinstance(cb, list):
+        cb = {(a, b): v for a, b, v in cb}
+    cl = RC(meshes, cross_bw=cb, cross_latency=d["cluster"]["cross_latency"])
+    store = rbs(layers, cl, RCM(**d["model"]), imbalance_ratio=float(d["imbalance_ratio"]))
+    return store, rbc(layers, cl), d["num_microbatches"], d["epsilon"]
+
+
 def reference_impl():
-    """Returns (kind, timer) where timer(pool_subset, workers) runs the
-    reference's own per-candidate DP search on host threads."""
+    """Returns (label, kind, make) where make(name) -> (pool, one) and one(t)
+    runs the reference's own per-candidate DP search (dp_search) on a host
+    thread."""
     ref = os.path.join(REPO, "oracle", "_ref")
     if os.path.isdir(os.path.join(ref, "meshpipe")):
         sys.path.insert(0, ref)
         try:
             import meshpipe  # noqa: F401
             from meshpipe import BACKEND
-            from meshpipe.cluster import ClusterSpec as RC, DeviceMesh as RM
-            from meshpipe.model_graph import Layer as RL, LayerSequence as RS
             from meshpipe.planner import DpTables as RT, dp_search as rdp
-            from meshpipe.profiling import CostModel as RCM, boundary_costs as rbc
-            from meshpipe.profiling import build_store as rbs
 
             def make(name):
                 from paper_2509_24859_b200.workloads import instance_dict
 
-                d = instance_dict(name)
-                lay = d["layers"]
-                layers = RS(tuple(RL(i, i + 1, lay["flops"][i], lay["param_bytes"][i],
-                                     lay["boundary_bytes"][i], tuple(lay["signature"][i]))
-                                  for i in range(len(lay["flops"]))), ())
-                meshes = [RM(m["id"], m["hosts"], m["devices_per_host"], m["peak_flops"],
-                             m["mem_device"], m["intra_host_bw"], m["inter_host_bw"])
-                          for m in d["cluster"]["meshes"]]
-                cb = d["cluster"]["cross_bw"]
-                if isinstance(cb, list):
-                    cb = {(a, b): v for a, b, v in cb}
-                cl = RC(meshes, cross_bw=cb, cross_latency=d["cluster"]["cross_latency"])
-                store = rbs(layers, cl, RCM(**d["model"]), imbalance_ratio=float(d["imbalance_ratio"]))
-                costs = rbc(layers, cl)
+                store, costs, B, eps = _ref_types(instance_dict(name))
                 tables = RT(store, costs)
-                B = d["num_microbatches"]
 
                 def one(t):
-                    return rdp(store, costs, B, t, d["epsilon"], tables)
+                    return rdp(store, costs, B, t, eps, tables)
 
                 return store.feasible_t_values(), one
 
@@ -122,6 +127,73 @@ def reference_impl():
         return tb["pool"], one
 
     return "oracle port (C restatement)", "port", make
+
+
+def reference_search_time(name: str, workers: int, reps: int = 3) -> dict:
+    """the reference's own planner.search(store, costs,
+    B, workers=ncores), wall clock, best of `reps`; build_store excluded
+    (reported separately)."""
+    from meshpipe.planner import search as rsearch
+
+    from paper_2509_24859_b200.workloads import instance_dict
+
+    d = instance_dict(name)
+    t0 = time.perf_counter()
+    store, costs, B, eps = _ref_types(d)
+    store_s = time.perf_counter() - t0
+    best, plan = math.inf, None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        plan = rsearch(store, costs, B, epsilon=eps, workers=workers, batch_size=4)
+        best = min(best, time.perf_counter() - t0)
+    return {"search_time_s": best, "build_store_s": store_s, "workers": workers, "reps": reps,
+            "T*": plan.predicted_latency, "t_max": plan.t_max, "stages": plan.num_stages}
+
+
+_E_PLANS = None  # config E inputs, set before the worker pool forks
+
+
+def _config_e_chunk(args):
+    """One worker's share of config E on the reference: adaptive_counts ->
+    build_program -> build_dag -> simulate per plan (simulation.py:73-228)."""
+    lo, hi = args
+    from meshpipe.scheduling import adaptive_counts, build_program
+    from meshpipe.simulation import build_dag, simulate
+
+    f, b, c, S = _E_PLANS
+    mk = 0.0
+    for p in range(lo, hi):
+        s = int(S[p])
+        tf, tb, cm = list(f[p, :s]), list(b[p, :s]), list(c[p, :s - 1])
+        lc = adaptive_counts([x + y for x, y in zip(tf, tb)], cm, 0.05)
+        mk += simulate(build_dag(tf, tb, cm, build_program(lc, 128))).makespan
+    return hi - lo, mk
+
+
+def reference_config_e(workers: int, budget_s: float = 12.0) -> dict:
+    """SURVEY.md §8(d) CPU baseline 3: config E plans/s of the reference on
+    multiprocessing.Pool(ncores) (fork: the workers share the generated
+    plans), over a bounded prefix of the 10^6 seeded plans bench.py's own
+    arm simulates."""
+    global _E_PLANS
+    import multiprocessing as mp
+
+    from paper_2509_24859_b200.workloads import config_e
+
+    _E_PLANS = config_e(1_000_000)
+    t0 = time.perf_counter()
+    _config_e_chunk((0, 40))
+    per = (time.perf_counter() - t0) / 40
+    n = int(max(workers * 8, min(1_000_000, budget_s * workers / per)))
+    step = (n + workers - 1) // workers
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        t0 = time.perf_counter()
+        done = sum(k for k, _ in pool.map(_config_e_chunk,
+                                          [(a, min(n, a + step)) for a in range(0, n, step)]))
+        dt = time.perf_counter() - t0
+    return {"plans_per_s": done / dt, "plans": done, "seconds": dt, "processes": workers,
+            "sample": f"first {done} of the 10^6 seeded config-E plans (seed 24859, B=128)"}
 
 
 def time_reference(make, name, budget_s: float, workers: int):
@@ -161,6 +233,11 @@ def run_reference_arm(args):
         samples.append((k, n, dt))
     value = sum(vals) / len(vals)
     k, n, dt = samples[-1]
+    extras = {}
+    if kind == "reference" and not args.no_extras:
+        extras["search"] = {name: reference_search_time(name, cores)
+                            for name in ("C", args.config)}
+        extras["config_e"] = reference_config_e(cores)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -182,6 +259,7 @@ def run_reference_arm(args):
                                    f"ThreadPoolExecutor({cores}) over dp_search; "
                                    f"host: {cpu_model()}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        **extras,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -227,7 +305,7 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t.start()
@@ -249,22 +327,92 @@ class ClockSampler:
                 else None, "reasons": reasons, "samples": len(self.rows)}
 
 
-def fp64_peak(lib, torch, device) -> float:
-    """Measured DADD throughput (adds/s) of this GPU: hapt_fp64_probe."""
-    from paper_2509_24859_b200._lib import check, stream_ptr
+def kernel_roofline(args, lib, torch, device, step, flush, tables, store, mine, ms_per_step,
+                    clocks) -> dict:
+    """roofline of the dominant kernel (dp_relax / dp_relax_compact):
 
-    out = torch.zeros(1, dtype=torch.float64, device=device)
-    blocks, threads, iters = 148 * 16, 256, 4096
-    check(lib.hapt_fp64_probe(out.data_ptr(), blocks, threads, 64, stream_ptr()))
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    best = math.inf
-    for _ in range(3):
-        s.record()
-        check(lib.hapt_fp64_probe(out.data_ptr(), blocks, threads, iters, stream_ptr()))
-        e.record()
-        e.synchronize()
-        best = min(best, s.elapsed_time(e) * 1e-3)
-    return blocks * threads * iters * 8 / best
+    * duration: a second pass of `steps` steps with the library's kernel
+      timing on (hapt_prof_enable: CUDA events around every launch on its
+      stream, no programmatic dependent launch) -> mean launch duration and
+      the kernel's share of the step;
+    * achieved / frac: DRAM bytes per launch MEASURED by ncu on this kernel
+      generation (profiles/dp_relax_traffic.json, tools/ncu_traffic.py, must
+      carry this library's hapt_version) over that duration, against the
+      measured HBM peak -- the kernel is latency-bound, so this is small;
+    * issue / eligible warps: the same ncu captures;
+    * reference_work_speedup: SURVEY.md §8(d)'s reference work units (32 B
+      per DP cell and layer + 28 B per CSR entry, every candidate) at HBM peak
+      over the measured step -- how far below the reference's work the
+      executed algorithm is, NOT a bandwidth."""
+    import ctypes
+
+    import numpy as np
+
+    n_mine = len(mine)
+    ms = np.zeros(3)
+    cnt = np.zeros(3, dtype=np.int64)
+    lib.hapt_prof_enable(1)
+    try:
+        for i in range(max(3, args.steps)):
+            flush.fill_(i & 0xFF)
+            step()
+        torch.cuda.synchronize()
+    finally:
+        lib.hapt_prof_enable(0)
+    lib.hapt_prof_read(ms.ctypes.data_as(ctypes.c_void_p), cnt.ctypes.data_as(ctypes.c_void_p), 3)
+    relax_s = ms[0] * 1e-3 / max(1, cnt[0])
+    share = float(ms[0] / ms.sum()) if ms.sum() > 0 else None
+    peaks = {}
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_hz = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0) * 1e6
+    tr, stale = None, None
+    try:
+        with open(os.path.join(REPO, "profiles", "dp_relax_traffic.json")) as fh:
+            tr = json.load(fh)
+        if tr.get("hapt_version") != lib.hapt_version():
+            stale = f"traffic counters from library {tr.get('hapt_version')}, running {lib.hapt_version()}"
+        elif tr.get("config") != args.config:
+            stale = f"traffic counters of config {tr.get('config')}"
+    except (OSError, ValueError):
+        stale = "profiles/dp_relax_traffic.json missing"
+    Lr, G, s_max = tables.L, tables.G, tables.s_max
+    nnz = store.dev.nnz
+    ref_bytes = (s_max * 32 * (Lr + 2) * (G + 1) + 28 * nnz) * n_mine  # SURVEY §8(d), per step
+    out = {
+        "bound": "hbm",
+        "kernel": "dp_relax_compact / dp_relax (hapt_dp.cu)",
+        "achieved": None, "peak": hbm_peak, "unit": "GB/s", "frac": None, "traffic": None,
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+        "launch_s": relax_s, "launches_per_step": cnt[0] / max(3, args.steps),
+        "share_of_step": share,
+        "timing": "hapt_prof_enable pass: CUDA events around each launch on its stream "
+                  "(programmatic dependent launch off), same steps as the timed loop",
+        "limiter": "latency: long-scoreboard stalls on dependent loads (see issue / eligible)",
+        "reference_work_speedup": (ref_bytes / (hbm_peak * 1e9)) / (ms_per_step * 1e-3),
+        "reference_work_bytes_per_step": ref_bytes,
+    }
+    if tr is not None and stale is None:
+        scale = n_mine / tr["pool_candidates"]
+        traffic = tr["dram_bytes_per_launch"] * scale
+        achieved = traffic / relax_s / 1e9
+        out.update({
+            "achieved": achieved, "frac": achieved / hbm_peak, "traffic": traffic,
+            "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write.sum, mean over "
+                            "the sweep's relax launches, scaled to this rank's candidates)",
+            "issue_frac": tr["instructions_per_launch"] * scale / relax_s / (148 * 4 * sm_hz),
+            "l2_gbs": tr["l2_bytes_per_launch"] * scale / relax_s / 1e9,
+            "l1_gbs": tr["l1_bytes_per_launch"] * scale / relax_s / 1e9,
+            "ncu_full": tr.get("ncu_full"),
+            "source": "profiles/dp_relax_traffic.json (" + tr.get("source", "?") + ")",
+        })
+    else:
+        out["stale"] = stale
+    return out
 
 
 def main():
@@ -309,6 +457,7 @@ def main():
     P = len(pool_all)
     mine = np.arange(rank, P, world)
     tmax = torch.from_numpy(pool_all[mine]).to(device)
+    gidx = torch.from_numpy(mine.astype(np.int64)).to(device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
     s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -316,12 +465,11 @@ def main():
     def step():
         ftop, states = sw.sweep_device(tmax)
         tstar, best_s, winner = sw.select_device(ftop, tmax, B)
-        if sharding is not None:
-            w = int(winner.item())
-            sharding.allreduce_argmin(float(tstar[w]) if w >= 0 else math.inf,
-                                      int(mine[w]) if w >= 0 else -1)
+        if sharding is not None:  # device-side allreduce-argmin, no host sync
+            return sharding.allreduce_argmin_device(tstar, winner, gidx)
         return winner
 
+    clk = ClockSampler(local).__enter__()  # sampled from warm-up to the end of the timed steps
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -329,13 +477,13 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     n_launch0 = lib.hapt_launches()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)
-            s_ev[i].record()
-            step()
-            e_ev[i].record()
-        torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        s_ev[i].record()
+        step()
+        e_ev[i].record()
+    torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
     n_launched = lib.hapt_launches() - n_launch0  # library's own launch counter
     if world > 1:
         dist.barrier()
@@ -347,100 +495,8 @@ def main():
     dev_s = float(t.item())
     value = P * args.steps / dev_s
     ms_per_step = dev_s / args.steps * 1e3
-
-    # dominant kernel (dp_relax): per-launch duration from the same sweeps
-    Lr, G, s_max = tables.L, tables.G, tables.s_max
-    relax_launches = sum(1 for s in range(1, s_max + 1) if (Lr - s + 1) * (G - s + 1) > 0)
-    chunks = sw.last_chunks
-    launches_per_step = n_launched / args.steps
-    nnz = store.dev.nnz
-    n_mine = len(mine)
-    bytes_per_cand = s_max * 32 * (Lr + 2) * (G + 1) + 28 * nnz
-    trans = tables.transitions_per_sweep()
-    sweep_s = dev_s / args.steps  # ~all of the step is the relax launches
-    avg_launch_s = sweep_s / max(1, relax_launches * chunks)
-    bytes_per_launch = bytes_per_cand * n_mine / max(1, relax_launches * chunks)
-    peaks = {}
-    try:
-        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-    except OSError:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = bytes_per_launch / avg_launch_s / 1e9
-    fp64 = fp64_peak(lib, torch, device)
-    # measured DRAM bytes per dp_relax launch of this workload, from the ncu
-    # metrics pass committed under profiles/ (tools/ncu_traffic.py)
-    traffic = None
-    measured = None
-    try:
-        with open(os.path.join(REPO, "profiles", "dp_relax_traffic.json")) as fh:
-            tr = json.load(fh)
-        if tr.get("config") == args.config:
-            scale = n_mine / tr["pool_candidates"]
-            traffic = tr["dram_bytes_per_launch"] * scale
-            # what the executed kernel actually moves / issues per launch
-            # (ncu counters of the same workload) over the live launch time;
-            # issue peak = 148 SMs x 4 schedulers x 1 warp-inst/clk x max SM clock
-            issue_peak = 148 * 4 * 1.965e9
-            measured = {
-                "dram_gbs": traffic / avg_launch_s / 1e9,
-                "dram_frac": traffic / avg_launch_s / 1e9 / hbm_peak,
-                "l2_gbs": tr["l2_bytes_per_launch"] * scale / avg_launch_s / 1e9,
-                "l1_gbs": tr["l1_bytes_per_launch"] * scale / avg_launch_s / 1e9,
-                "warp_inst_per_s": tr["instructions_per_launch"] * scale / avg_launch_s,
-                "issue_frac": tr["instructions_per_launch"] * scale / avg_launch_s / issue_peak,
-                "source": "profiles/dp_relax_traffic.json (" + tr.get("source", "?") + ")",
-            }
-    except (OSError, KeyError, ValueError):
-        pass
-    # the transitions the kernel actually executes (instrumented build,
-    # tools/work_counts.py: a property of the algorithm, scaled to this run)
-    try:
-        with open(os.path.join(REPO, "profiles", "dp_relax_work.json")) as fh:
-            wk = json.load(fh)[args.config]
-        if measured is not None:
-            scale = n_mine / wk["pool_candidates"]
-            ex = wk["executed_lane_transitions"] * scale * args.steps / dev_s
-            measured.update({
-                "executed_transitions_per_s": ex,
-                "executed_share_of_reference_transitions":
-                    wk["executed_lane_transitions"] / wk["reference_transitions"],
-                "admissible_share_of_executed":
-                    wk["admissible_lane_transitions"] / wk["executed_lane_transitions"],
-                "executed_fp64_frac": 2 * ex / fp64,  # one DADD + one compare each
-            })
-    except (OSError, KeyError, ValueError):
-        pass
-    roofline = {
-        "bound": "hbm",
-        "kernel": "dp_relax (hapt_dp.cu)",
-        "achieved": achieved,
-        "peak": hbm_peak,
-        "unit": "GB/s",
-        "frac": achieved / hbm_peak,
-        "traffic": traffic,
-        "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write, mean over a sweep)",
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-        "algorithmic_bytes_per_candidate": bytes_per_cand,
-        "work_units": "reference",
-        "note": ("achieved/frac count SURVEY.md 8(d)'s reference work (32 B/cell F,N,"
-                 "bp layout, every CSR transition); the kernel stores 10 B/cell and skips "
-                 "provably infeasible transitions/cells and the transitions a warp-wide "
-                 "lower bound proves non-improving (0.7-1.2 % of the reference's are "
-                 "executed), so frac > 1 is algorithmic saving, "
-                 "not a measurement error; 'measured' is the executed kernel's own "
-                 "DRAM/L2/issue rate"),
-        "measured": measured,
-        "fp64": {
-            "ops_per_candidate": 2 * trans,
-            "achieved_ops_s": 2 * trans * n_mine * args.steps / dev_s,
-            "measured_dadd_peak_ops_s": fp64,
-            "frac": (2 * trans * n_mine * args.steps / dev_s) / fp64,
-            "transitions_per_s": trans * n_mine * args.steps / dev_s,
-            "dp_cells_per_s": s_max * Lr * G * n_mine * args.steps / dev_s,
-        },
-    }
+    roofline = kernel_roofline(args, lib, torch, device, step, flush, tables, store, mine,
+                               ms_per_step, clk.summary())
 
     # e2e through the public API from host inputs (rank-sharded when N>1).
     # Long-lived interpreter objects (torch, numpy, the loaded instance) are
@@ -452,7 +508,7 @@ def main():
     gc.collect()
     gc.freeze()
     e2e_times = []
-    h2d = 8 * (3 * Lr + 4 * len(cluster.meshes)) + 4 * (Lr + 2 * len(cluster.meshes) + 3 * len(store.options))
+    h2d = d2h = 0
     for i in range(2 + args.steps):
         flush.fill_(i & 0xFF)
         torch.cuda.synchronize()
@@ -466,21 +522,31 @@ def main():
         dt = time.perf_counter() - t0
         if i >= 2:
             e2e_times.append(dt)
-    d2h = 8 * 16 + P * 8 + P * (8 + 8 + 8) // max(1, world)
+        # bytes copied per step: the instance description (one H2D blob),
+        # the K1 counters, and the results (pool, T*, best s, finite cells,
+        # winner; with N > 1 each rank's share plus the all_gathered results)
+        h2d = st2.dev.h2d_bytes
+        d2h = 16 * 8 + (P * 8 * 4 + 8 if world == 1 else P * 8 + (P * 24 + 8 * world))
     t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_value = P * len(e2e_times) / float(t.item())
     assert int(win_r) >= 0
 
-    # planner search time: search() end to end
-    search_times = []
+    # planner search time: search() end to end, and search() on a prebuilt
+    # store (the reference arm's search_time_s excludes build_store)
+    search_times, search_only = [], []
     for i in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st3 = build_store(layers, cluster, model, imbalance_ratio=rho)
-        plan = search(st3, boundary_costs(layers, cluster), B, epsilon=eps, dist=sharding)
-        search_times.append(time.perf_counter() - t0)
+        c3 = boundary_costs(layers, cluster)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        plan = search(st3, c3, B, epsilon=eps, dist=sharding)
+        t2 = time.perf_counter()
+        search_times.append(t2 - t0)
+        search_only.append(t2 - t1)
     search_time = min(search_times)
 
     line = {
@@ -496,14 +562,17 @@ def main():
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {**workload_config(args), "pool_candidates": P, "layers": Lr, "devices": G,
-                   "s_max": s_max, "transitions_per_sweep": trans, "nnz": nnz},
+        "config": {**workload_config(args), "pool_candidates": P, "layers": tables.L,
+                   "devices": tables.G, "s_max": tables.s_max,
+                   "transitions_per_sweep": tables.transitions_per_sweep(),
+                   "nnz": store.dev.nnz},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "build_store -> boundary_costs -> planner.sweep_pool (host in, host out)",
                 "host_gc": "gc.freeze() after warm-up"},
         "search_time_s": search_time,
+        "search_only_s": min(search_only),
         "search_plan": {"stages": plan.num_stages, "T*": plan.predicted_latency,
                         "t_max": plan.t_max, "evaluated": plan.search_stats["evaluated"]},
         "gpu_launches": n_launched,

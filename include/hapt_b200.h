@@ -337,6 +337,15 @@ int hapt_dag_asap_check(int32_t n_nodes, const int32_t *succ_off, const int32_t 
                         double rel_tol, int32_t *first_bad, void *work, size_t work_bytes,
                         void *stream);
 
+/* Kernel timing for measurement (bench.py): while enabled, every DP sweep
+ * launch is bracketed by CUDA events on its stream (and programmatic
+ * dependent launch is off, so each interval is one kernel).  hapt_prof_read
+ * synchronises, returns per kind (0 = dp_relax / dp_relax_compact, 1 =
+ * dp_window, 2 = the rest of the sweep) the summed milliseconds and launch
+ * counts since the last read, and resets. */
+int hapt_prof_enable(int32_t on);
+int hapt_prof_read(double *ms, int64_t *count, int32_t n_kinds);
+
 /* Longest-path start times of an arbitrary DAG given as successor CSR:
  * start[v] = max_u (start[u] + duration[u]). processed [1] = number of nodes
  * reached (< n_nodes <=> cycle). */

@@ -164,6 +164,8 @@ _SIGNATURES = {
         [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
          c_vp, c_vp, c_vp],
     ),
+    "hapt_prof_enable": (c_i32, [c_i32]),
+    "hapt_prof_read": (c_i32, [c_vp, c_vp, c_i32]),
     "hapt_steady_rate_1f1b": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "hapt_asap_workspace_bytes": (c_sz, [c_i32]),
     "hapt_dag_asap_check": (

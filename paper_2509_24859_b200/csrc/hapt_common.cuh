@@ -54,6 +54,18 @@ __device__ __forceinline__ void pdl_trigger() {
 
 bool pdl_enabled();  // HAPT_PDL=0 disables (A/B measurements)
 
+// Kernel timing (hapt_prof_enable / hapt_prof_read): kinds of timed launches
+enum ProfKind { kProfRelax = 0, kProfWindow = 1, kProfOther = 2, kProfKinds = 3 };
+bool prof_on();
+void *prof_begin(int kind, cudaStream_t st);
+void prof_end(void *h, cudaStream_t st);
+struct ProfScope {
+  void *h;
+  cudaStream_t st;
+  ProfScope(int kind, cudaStream_t s) : h(prof_begin(kind, s)), st(s) {}
+  ~ProfScope() { prof_end(h, st); }
+};
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, bool on,
                        Args... args) {

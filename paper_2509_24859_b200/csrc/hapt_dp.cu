@@ -49,9 +49,6 @@ constexpr int kChunk = HAPT_CHUNK;
 #ifndef HAPT_WIN_MINLEN
 #define HAPT_WIN_MINLEN 1  // window hull also bounded by each option's shortest span
 #endif  // window cells of one (group, state) per relax warp
-#ifndef HAPT_RELAX_WARPLOOP
-#define HAPT_RELAX_WARPLOOP 1  // 0: units of kWarps cells with block barriers (v14)
-#endif
 #ifndef HAPT_RELAX_MINB
 #define HAPT_RELAX_MINB 8  // resident blocks/SM (64 registers at 4 warps per block)
 #endif
@@ -1184,14 +1181,34 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
 // the device, so the launch gap overlaps the previous kernel's tail).
 int run_sweep(const Batch &b, cudaStream_t st) {
   // measured: on tiny tables (config A, L*G ~ 100) the dependent-launch wait
-  // costs more than the gap it hides
-  const bool pdl = pdl_enabled() && (long)b.L * b.G >= 4096;
+  // costs more than the gap it hides; kernel timing (prof_on) brackets every
+  // launch with events, so it runs without PDL
+  const bool pdl = pdl_enabled() && (long)b.L * b.G >= 4096 && !prof_on();
   const int n_span = 2 * b.n_groups * b.n_opts;
-  HAPT_CUDA(launch_pdl(dp_ftop_init,
-                       grid_for(max((size_t)b.n_cand * (b.s_max + 1), (size_t)n_span), 256), 256,
-                       st, pdl, b.ftop, b.states, b.n_cand, b.s_max, b.spanlen, n_span));
-  // block >= 128 = max group width
-  HAPT_CUDA(launch_pdl(dp_prep, dim3(b.n_groups, kPrepY), 256, st, pdl, b));
+  {
+    ProfScope ps(kProfOther, st);
+    HAPT_CUDA(launch_pdl(dp_ftop_init,
+                         grid_for(max((size_t)b.n_cand * (b.s_max + 1), (size_t)n_span), 256),
+                         256, st, pdl, b.ftop, b.states, b.n_cand, b.s_max, b.spanlen, n_span));
+  }
+  {
+    ProfScope ps(kProfOther, st);  // block >= 128 = max group width
+    HAPT_CUDA(launch_pdl(dp_prep, dim3(b.n_groups, kPrepY), 256, st, pdl, b));
+  }
+  // grid cap of dp_relax_compact: 256 warps per SM, per device
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned gcap = (256u / kWarps) * (unsigned)sms;
+  if (const char *e = getenv("HAPT_RELAX_GRID")) {
+    const long v = atol(e);
+    if (v >= 1 && v <= (1l << 20)) gcap = (unsigned)v;
+  }
+  static const long win_min = [] {
+    const char *e = getenv("HAPT_WINDOW_MIN");
+    const long v = e ? atol(e) : 32768;
+    return v >= 0 ? v : 32768;
+  }();
   for (int s = 1; s <= b.s_max; ++s) {
     const long cells = (long)(b.L - s + 1) * (b.G - s + 1);
     if (cells <= 0) break;
@@ -1200,25 +1217,20 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     const unsigned long long magic = ((1ull << 32) + nk - 1) / nk;  // ceil(2^32 / nk)
     // the window pass pays off once the layer has far more warps than the
     // GPU holds at once; on small grids its launch costs more than it saves
-    static const long win_min = getenv("HAPT_WINDOW_MIN") ? atol(getenv("HAPT_WINDOW_MIN"))
-                                                          : 32768;
     const int use_window = cells * b.n_groups >= win_min;
     if (use_window) {
       const dim3 wgrid((b.G + 1 + kWinWarps - 1) / kWinWarps, b.n_groups);
-      HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinWarps * 32, st, pdl, b, s));
+      {
+        ProfScope ps(kProfWindow, st);
+        HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinWarps * 32, st, pdl, b, s));
+      }
       // the compact list's length is only known on the device: the grid is
       // its upper bound, capped at 256 warps per SM that loop over the cells
       // (measured: launching the bound's mostly empty blocks cost ~4 % of a
       // D1 pool sweep; 128 warps per SM: +2.5 %, 512: +2.6 % at kWarps 8)
-      static const unsigned gcap = [] {
-        if (const char *e = getenv("HAPT_RELAX_GRID")) return (unsigned)atoi(e);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        return (256u / kWarps) * (unsigned)sms;
-      }();
       const unsigned cgrid = min(gcap, grid_for((size_t)cells * b.n_groups, kWarps));
       const dim3 blk(kWarps * 32);
+      ProfScope ps(kProfRelax, st);
       if (b.cpl == 1)
         HAPT_CUDA(launch_pdl(dp_relax_compact<1>, cgrid, blk, st, pdl, b, s));
       else if (b.cpl == 2)
@@ -1229,6 +1241,7 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     }
     for (int g0 = 0; g0 < b.n_groups; g0 += 65535) {
       const dim3 grid(gx, min(65535, b.n_groups - g0)), blk(kWarps * 32);
+      ProfScope ps(kProfRelax, st);
       if (b.cpl == 1)
         HAPT_CUDA(launch_pdl(dp_relax<1>, grid, blk, st, pdl, b, s, g0, magic));
       else if (b.cpl == 2)
@@ -1237,6 +1250,7 @@ int run_sweep(const Batch &b, cudaStream_t st) {
         HAPT_CUDA(launch_pdl(dp_relax<4>, grid, blk, st, pdl, b, s, g0, magic));
     }
   }
+  ProfScope ps(kProfOther, st);
   HAPT_CUDA(launch_pdl(dp_states_reduce, grid_for(b.n_cand, 256), 256, st, pdl, b));
   return HAPT_OK;
 }

@@ -5,6 +5,8 @@
 #include <stdlib.h>
 
 #include <atomic>
+#include <mutex>
+#include <vector>
 
 #include "hapt_common.cuh"
 
@@ -31,6 +33,46 @@ bool pdl_enabled() {
   return on;
 }
 
+// Kernel timing (bench.py's per-kernel roofline figures): while enabled, the
+// sweep brackets each launch with a pair of CUDA events on its stream and
+// disables programmatic dependent launch, so every interval is one kernel.
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_prof_free;
+
+bool prof_on() { return g_prof_on; }
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_free.empty()) {
+    cudaEvent_t e = g_prof_free.back();
+    g_prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void *prof_begin(int kind, cudaStream_t st) {
+  if (!g_prof_on) return nullptr;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfRec r{kind, prof_event(), prof_event()};
+  cudaEventRecord(r.a, st);
+  g_prof.push_back(r);
+  return (void *)(g_prof.size());  // 1-based handle
+}
+
+void prof_end(void *h, cudaStream_t st) {
+  if (!h) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEventRecord(g_prof[(size_t)h - 1].b, st);
+}
+
 namespace {
 // 8 independent DADD chains per thread; iters * 8 adds per thread.
 __global__ void k_fp64_probe(double *out, int iters) {
@@ -52,7 +94,36 @@ using namespace hapt;
 
 extern "C" const char *hapt_last_error(void) { return g_err; }
 
-extern "C" int hapt_version(void) { return 10000; }
+// 1 0 0 18: ABI 1, DP kernel generation 18 (profiles/dp_relax_traffic.json
+// records the generation its counters were taken on)
+extern "C" int hapt_version(void) { return 10018; }
+
+extern "C" int hapt_prof_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  return HAPT_OK;
+}
+
+extern "C" int hapt_prof_read(double *ms, int64_t *count, int32_t n_kinds) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int k = 0; k < n_kinds; ++k) {
+    ms[k] = 0.0;
+    count[k] = 0;
+  }
+  for (const ProfRec &r : g_prof) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+      return cuda_status(cudaGetLastError(), "hapt_prof_read");
+    if (r.kind >= 0 && r.kind < n_kinds) {
+      ms[r.kind] += t;
+      count[r.kind] += 1;
+    }
+    g_prof_free.push_back(r.a);
+    g_prof_free.push_back(r.b);
+  }
+  g_prof.clear();
+  return HAPT_OK;
+}
 
 extern "C" int64_t hapt_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 

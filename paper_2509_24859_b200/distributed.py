@@ -26,7 +26,14 @@ _I64_MAX = np.iinfo(np.int64).max
 
 
 class PoolSharding:
-    def __init__(self, group=None):
+    """min_shard: batches smaller than this are evaluated whole on every rank
+    (identical results, no collective) -- a small probe batch does not fill
+    one GPU, so splitting it only adds an all_gather to its latency."""
+
+    MIN_SHARD = 1024
+
+    def __init__(self, group=None, min_shard: int | None = None):
+        self.min_shard = self.MIN_SHARD if min_shard is None else int(min_shard)
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed is not initialised")
         self.group = group
@@ -89,6 +96,36 @@ class PoolSharding:
         if want_ftop:
             return tstar, best_s, states, ftop
         return tstar, best_s, states
+
+    def allreduce_argmin_device(self, tstar: torch.Tensor, winner: torch.Tensor,
+                                global_index: torch.Tensor):
+        """Device-side allreduce-argmin of a sweep's local winner, no host
+        synchronisation: tstar [n] float64 and winner [1] int32 as
+        hapt_dp_select returns them (winner -1: nothing feasible here),
+        global_index [n] int64 the candidates' pool indices.  One all_gather
+        of a 16-byte (bits(T*), index) key per rank, then the lexicographic
+        minimum on the device (non-negative IEEE doubles order like their
+        bit patterns).  Returns (bits of the global T* [int64, I64_MAX if
+        none], its pool index [int64, I64_MAX if none]) as device tensors."""
+        dev = self.device
+        w = winner.to(device=dev, dtype=torch.int64).reshape(1)
+        ok = w >= 0
+        wi = w.clamp(min=0)
+        big = torch.full((1,), _I64_MAX, dtype=torch.int64, device=dev)
+        bits = torch.where(ok, tstar.to(dev).view(torch.int64)[wi], big)
+        gi = torch.where(ok, global_index.to(dev)[wi], big)
+        loc = torch.cat([bits, gi]).reshape(1, 2)
+        if self.backend == "nccl":
+            out = torch.empty((self.world, 2), dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(out, loc, group=self.group)
+        else:
+            parts = [torch.empty_like(loc) for _ in range(self.world)]
+            dist.all_gather(parts, loc, group=self.group)
+            out = torch.cat(parts)
+        self.collective_calls += 1
+        gbits = out[:, 0].min()
+        gidx = torch.where(out[:, 0] == gbits, out[:, 1], big.expand(self.world)).min()
+        return gbits, gidx
 
     def allreduce_argmin(self, tstar: float, index: int):
         """Global lexicographic min of (T*, index) over ranks; (inf, -1) if

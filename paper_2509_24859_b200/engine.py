@@ -94,6 +94,7 @@ class DeviceTables:
         for off, raw in parts:
             host[off : off + raw.size] = raw
         blob = torch.from_numpy(host).to(dev)
+        self.h2d_bytes = int(host.nbytes)  # bench.py's e2e accounting
         base = blob.data_ptr()
         for name in desc_arrays:
             setattr(d, name, base + offs[name] if name in offs else None)

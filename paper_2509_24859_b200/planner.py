@@ -273,7 +273,9 @@ class CandidateEvaluator:
             return
         self.batches += 1
         self.evaluated += len(todo)
-        if self.dist is None:
+        if self.dist is None or len(todo) < self.dist.min_shard:
+            # single GPU, or a batch too small to split (replicated on every
+            # rank: identical results, no collective)
             sw = self.tables.sweeper
             need = sw.bp_bytes(len(todo))
             keep = keep_bp and self._bp_bytes + need <= sw.BP_BUDGET
@@ -611,8 +613,24 @@ def search(store: ProfileStore, costs: BoundaryCost, num_microbatches: int,
 
 def sweep_pool(store: ProfileStore, costs: BoundaryCost, num_microbatches: int, dist=None):
     """Evaluate EVERY t_max candidate of the pool in one batched sweep (the
-    candidates/s workload).  Returns (pool, tstar, best_s, states, winner)."""
+    candidates/s workload).  Returns (pool, tstar, best_s, states, winner).
+    On one GPU the pool never leaves the device before the sweep (K1 writes
+    it, K2 reads it) and all results come back in one transfer."""
     tables = DpTables(store, costs)
+    if dist is None:
+        import torch
+
+        if store.dev.pool_len == 0:
+            raise InfeasiblePlanError("no feasible candidates in the profile store")
+        sw = tables.sweeper
+        pool_dev = store.dev.pool()
+        ftop, states = sw.sweep_device(pool_dev)
+        tstar, best_s, winner = sw.select_device(ftop, pool_dev, num_microbatches)
+        n = int(pool_dev.numel())
+        host = torch.cat([pool_dev.view(torch.int64), tstar.view(torch.int64),
+                          best_s.to(torch.int64), states, winner.to(torch.int64)]).cpu().numpy()
+        return (host[:n].view(np.float64).copy(), host[n:2 * n].view(np.float64).copy(),
+                host[2 * n:3 * n].copy(), host[3 * n:4 * n].copy(), int(host[4 * n]))
     pool = candidate_tmax(store)
     ev = CandidateEvaluator(tables, pool, num_microbatches, dist)
     ev.ensure(range(len(pool)), keep_bp=False)  # no plan is built from a pool sweep

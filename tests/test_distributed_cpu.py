@@ -21,7 +21,12 @@ class OracleSweeper:
         self.inst, self.tb = inst, tb
         self.calls = []
 
-    def evaluate(self, tmax_values, B):
+    BP_BUDGET = 0  # keeps no backpointers (plans are not built here)
+
+    def bp_bytes(self, n):
+        return 1
+
+    def evaluate(self, tmax_values, B, keep_bp=False, keep_ftop=False):
         import oracle as O
         from paper_2509_24859_b200.engine import SweepResult
 
@@ -33,7 +38,7 @@ class OracleSweeper:
         return SweepResult(t, ts, bs.astype(np.int64), st, winner)
 
 
-def _worker(rank, world, port, name, out_q):
+def _worker(rank, world, port, name, out_q, min_shard):
     sys.path.insert(0, os.path.dirname(HERE))
     sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
     sys.path.insert(0, HERE)
@@ -52,7 +57,7 @@ def _worker(rank, world, port, name, out_q):
         tb = O.tables(inst)
         pool = tb["pool"]
         B = inst["num_microbatches"]
-        sh = PoolSharding()
+        sh = PoolSharding(min_shard=min_shard)
         sw = OracleSweeper(inst, tb)
 
         class Tables:
@@ -70,8 +75,15 @@ def _worker(rank, world, port, name, out_q):
         w = res.winner
         g_t, g_i = sh.allreduce_argmin(float(res.tstar[w]) if w >= 0 else float("inf"),
                                        mine[w] if w >= 0 else -1)
+        # the device-tensor variant bench.py uses (no host sync; CPU tensors on gloo)
+        import torch
+
+        d_bits, d_idx = sh.allreduce_argmin_device(
+            torch.from_numpy(np.ascontiguousarray(res.tstar, dtype=np.float64)),
+            torch.tensor([w], dtype=torch.int32), torch.tensor(mine, dtype=torch.int64))
+        d_t = float(np.array([int(d_bits)], dtype=np.int64).view(np.float64)[0])
         out_q.put((rank, lo, surv, best, float(ev.tstar[best]), g_t, g_i, sum(sw.calls),
-                   sh.collective_calls))
+                   sh.collective_calls, d_t, int(d_idx)))
     finally:
         dist.destroy_process_group()
 
@@ -82,15 +94,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name", ["A", "B"])
-def test_two_rank_search_and_argmin(name):
+@pytest.mark.parametrize("name,min_shard", [("A", 1), ("B", 1), ("B", 10 ** 6)])
+def test_two_rank_search_and_argmin(name, min_shard):
+    """min_shard=1 shards every batch; 10**6 replicates them all (only the
+    full-pool argmin exchanges data)."""
     import oracle as O
     from helpers import expected, expected_arrays, load_json
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q, min_shard))
+             for r in range(2)]
     for p in procs:
         p.start()
     results = sorted(q.get(timeout=300) for _ in procs)
@@ -101,7 +116,7 @@ def test_two_rank_search_and_argmin(name):
     arr = expected_arrays(name)
     pool = arr["pool"]
     ref_plan = exp["plan"]
-    for rank, lo, surv, best, tstar, g_t, g_i, n_eval, n_coll in results:
+    for rank, lo, surv, best, tstar, g_t, g_i, n_eval, n_coll, d_t, d_i in results:
         assert tstar == ref_plan["predicted_latency"]
         assert pool[best] == ref_plan["t_max"]
         assert lo == ref_plan["search_stats"]["pruned_below_ts"]
@@ -109,7 +124,8 @@ def test_two_rank_search_and_argmin(name):
         feas = np.where(arr["best_s"] >= 0)[0]
         win = feas[np.lexsort((pool[feas], arr["tstar"][feas]))[0]]
         assert (g_t, g_i) == (float(arr["tstar"][win]), int(win))
-        assert n_coll >= 3
+        assert (d_t, d_i) == (g_t, g_i)
+        assert n_coll >= (4 if min_shard == 1 else 3)
     # every pool candidate evaluated exactly once across the two ranks
     assert results[0][7] + results[1][7] >= len(O.tables(load_json(name))["pool"])
     assert results[0][1:7] == results[1][1:7]

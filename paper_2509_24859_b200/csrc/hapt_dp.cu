@@ -731,55 +731,62 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   }
   // epilogue per candidate
   double hn[CPL];
-  int kn[CPL];
+  int kn[CPL], bkk[CPL];
   const int crow = gm.w;
   const double c2 = crow >= 0 ? __dmul_rn(2.0, b.cb[(size_t)crow * (L + 1) + (k - 1)]) : 0.0;
   const uint8_t *kcp = b.kc + ((size_t)group * b.cb_rows + (crow >= 0 ? crow : 0)) * (L + 1) * CW +
                        (size_t)(k - 1) * CW + lane * CPL;
-  // warp-uniform: backpointers / F / N are only recorded when a caller asked
-  const bool want_bp = b.full.bp_packed != nullptr || b.full.bp_o != nullptr;
-  const bool top = k == 1 && g == G;
-  // the CPL launch-bound increments of this lane in one load
+  // the CPL launch-bound increments of this lane in one load (0xFF: c > t_max)
   unsigned kcw = 0xFFFFFFFFu;
   if (crow >= 0) {
     if constexpr (CPL == 4) kcw = __ldg(reinterpret_cast<const unsigned *>(kcp));
-    else if constexpr (CPL == 2) kcw = __ldg(reinterpret_cast<const uint16_t *>(kcp));
-    else kcw = __ldg(kcp);
+    else if constexpr (CPL == 2) kcw = 0xFFFF0000u | __ldg(reinterpret_cast<const uint16_t *>(kcp));
+    else kcw = 0xFFFFFF00u | __ldg(kcp);
   }
+  // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
+  // (the successor's K slot is at byte offset bw3 / 4 from Kb)
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     fin[c] = bv[c] < kInf;
-    const double best = bv[c];
-    const unsigned boff = bw3[c] / (256u * CPL);
-    // N of the winner = its KK (_dp.pyx:87); reloaded once instead of tracked
-    const int bkk = fin[c] ? (int)__ldg(Kg + (size_t)boff * CW + c) : 0;
-    const int cand = cand0 + c;
-    if (top && cand < b.n_cand) {
-      b.ftop[(size_t)cand * (b.s_max + 1) + s] = best;
-      if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk;
+    bkk[c] = fin[c] ? (int)__ldg(reinterpret_cast<const uint16_t *>(Kb + (bw3[c] >> 2)) + c) : 0;
+  }
+  if (k == 1 && g == G) {  // warp-uniform: the top cell F[s,1,G] of every candidate
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int cand = cand0 + c;
+      if (cand >= b.n_cand) continue;
+      b.ftop[(size_t)cand * (b.s_max + 1) + s] = bv[c];
+      if (b.full.ntop) b.full.ntop[(size_t)cand * (b.s_max + 1) + s] = bkk[c];
     }
-    if (want_bp && fin[c] && cand < b.n_cand) {
-      const int g2 = (int)boff / (L + 1), bi = (int)boff - g2 * (L + 1);
-      const int bo = winner_option(b.opt_devs, b.span_off, b.spans, L, k, g - g2, bi, best,
-                                   cnt[c], bkk, __ldg(Hg + (size_t)boff * CW + c), gm.x, gm.y);
+  }
+  // warp-uniform: backpointers / F / N are only recorded when a caller asked
+  if (b.full.bp_packed != nullptr || b.full.bp_o != nullptr) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int cand = cand0 + c;
+      if (!fin[c] || cand >= b.n_cand) continue;
+      const int boff = (int)(bw3[c] / (256u * CPL));
+      const int g2 = boff / (L + 1), bi = boff - g2 * (L + 1);
+      const int bo = winner_option(b.opt_devs, b.span_off, b.spans, L, k, g - g2, bi, bv[c],
+                                   cnt[c], bkk[c], __ldg(Hg + (size_t)boff * CW + c), gm.x, gm.y);
       const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
       if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
       if (b.full.bp_o) {
-        if (b.full.F) b.full.F[e] = best;
-        if (b.full.N) b.full.N[e] = (double)bkk;
+        if (b.full.F) b.full.F[e] = bv[c];
+        if (b.full.N) b.full.N[e] = (double)bkk[c];
         b.full.bp_i[e] = bi;
         b.full.bp_o[e] = bo;
       }
     }
-    // successor entry (state g, split i = k-1) for layer s+1:
-    // H = 2c + F, KK = (ceil(2c/t_max) + 1) + N, or +inf if c > t_max
-    hn[c] = kInf;
-    kn[c] = 0;
-    const int kcv = crow >= 0 ? (int)((kcw >> (8 * c)) & 0xFFu) : 0xFF;
-    if (fin[c] && kcv != 0xFF) {
-      hn[c] = __dadd_rn(c2, best);
-      kn[c] = kcv + bkk;
-    }
+  }
+  // successor entry (state g, split i = k-1) for layer s+1:
+  // H = 2c + F, KK = (ceil(2c/t_max) + 1) + N, or +inf if c > t_max
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int kcv = (int)((kcw >> (8 * c)) & 0xFFu);
+    const bool ok = fin[c] && kcv != 0xFF;
+    hn[c] = ok ? __dadd_rn(c2, bv[c]) : kInf;
+    kn[c] = ok ? kcv + bkk[c] : 0;
   }
   const size_t o_idx = hm_idx * CW + lane * CPL;
   bool anyfin = false;

@@ -552,7 +552,7 @@ template <int CPL>
 __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int k, int g,
                                            int lane, int4 *__restrict__ stage_e,
                                            uint16_t *__restrict__ stage_k, int (&fin)[CPL],
-                                           const int4 gm, const OptLane &ol0) {
+                                           const int o0, const int nopt, const OptLane &ol0) {
   constexpr int CW = 32 * CPL;
   const int L = b.L, G = b.G;
   const int cand0 = group * CW + lane * CPL;
@@ -560,7 +560,6 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
 #pragma unroll
   for (int c = 0; c < CPL; ++c) cnt[c] = (unsigned)b.tcnt[cand0 + c];
   const int imax = L - s + 1;
-  const int o0 = gm.x, nopt = gm.y, avail = gm.z;
   const size_t gbase = (size_t)group * b.hg;
   const double *Hg = b.H[(s - 1) & 1] + gbase * CW + lane * CPL;
   const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * CW + lane * CPL;
@@ -575,10 +574,11 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   }
   // options of mesh r, 32 at a time (a mesh rarely has more than 32 submesh
   // shapes); rows are visited in ascending option order
-  for (int c0 = 0; c0 < nopt; c0 += 32) {
+  // (one chunk in practice: the second and later only for meshes with more
+  // than 32 shapes, so nothing of the chunk loop stays live in the main path)
+  auto chunk = [&](const int c0, const OptLane &ol) {
     const int nch = min(32, nopt - c0);
     const int o = o0 + c0 + lane;
-    const OptLane ol = c0 == 0 ? ol0 : opt_lane(b, s, group, g, o, avail, lane < nch);
     // lane j: admissible entries of option o's row (k) at this layer
     int len = 0, beg = 0;
     bool needkk = false;
@@ -707,6 +707,12 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
         relax_entries<false, CPL>(stage_e, stage_k, n, cnt, Hb, Kb, bv, bw3);
       __syncwarp();
     }
+  };
+  chunk(0, ol0);
+  if (nopt > 32) {
+    const int avail = b.gmeta[g].z;
+    for (int c0 = 32; c0 < nopt; c0 += 32)
+      chunk(c0, opt_lane(b, s, group, g, o0 + c0 + lane, avail, lane < min(32, nopt - c0)));
   }
   // A warp with no finite best records nothing, and its successor entry is
   // infinite for every lane: only Hmin = +inf is written, which makes the
@@ -732,7 +738,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   // epilogue per candidate
   double hn[CPL];
   int kn[CPL], bkk[CPL];
-  const int crow = gm.w;
+  const int crow = __ldg(&b.gmeta[g].w);  // successor boundary row of state g
   const double c2 = crow >= 0 ? __dmul_rn(2.0, b.cb[(size_t)crow * (L + 1) + (k - 1)]) : 0.0;
   const uint8_t *kcp = b.kc + ((size_t)group * b.cb_rows + (crow >= 0 ? crow : 0)) * (L + 1) * CW +
                        (size_t)(k - 1) * CW + lane * CPL;
@@ -768,7 +774,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       const int boff = (int)(bw3[c] / (256u * CPL));
       const int g2 = boff / (L + 1), bi = boff - g2 * (L + 1);
       const int bo = winner_option(b.opt_devs, b.span_off, b.spans, L, k, g - g2, bi, bv[c],
-                                   cnt[c], bkk[c], __ldg(Hg + (size_t)boff * CW + c), gm.x, gm.y);
+                                   cnt[c], bkk[c], __ldg(Hg + (size_t)boff * CW + c), o0, nopt);
       const size_t e = (((size_t)cand * (b.s_max + 1) + s) * (L + 2) + k) * (G + 1) + g;
       if (b.full.bp_packed) b.full.bp_packed[e] = (bo << 16) | bi;
       if (b.full.bp_o) {
@@ -849,7 +855,8 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   if (active) {
     const int4 gm = b.gmeta[g];
     const OptLane ol0 = opt_lane(b, s, group, g, gm.x + lane, gm.z, lane < gm.y);
-    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm, ol0);
+    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm.x, gm.y,
+                    ol0);
   }
   if (blockIdx.x == 0) {  // the buffer layer s+1 writes: last read by layer s-1
     for (int x = threadIdx.x; x <= G; x += blockDim.x)
@@ -941,7 +948,8 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     }
     for (int k = k0; k <= k1; ++k) {
       int fin[CPL];
-      relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm, ol0);
+      relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm.x, gm.y,
+                      ol0);
 #pragma unroll
       for (int c = 0; c < CPL; ++c) cnt[c] += fin[c] ? 1u : 0u;
     }

@@ -42,10 +42,6 @@ __device__ unsigned long long g_work[8];  // executed / admissible / improving l
 #endif
 constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
-#ifndef HAPT_CHUNK
-#define HAPT_CHUNK 1
-#endif
-constexpr int kChunk = HAPT_CHUNK;
 #ifndef HAPT_WIN_MINLEN
 #define HAPT_WIN_MINLEN 1  // window hull also bounded by each option's shortest span
 #endif  // window cells of one (group, state) per relax warp
@@ -121,13 +117,11 @@ struct Batch {
                        // layer s reads [(s-1)%3], writes [s%3], resets [(s+1)%3]
   uint32_t *spanlen;   // [n_groups][2][n_opts] 0xffff - shortest, longest admissible
                        // span length of an option (before the group's cut)
-  uint16_t *winhi;     // [n_groups][G+1] last k of state g's window (dp_window)
   int2 *wopt;          // [n_groups][G+1][32] per state and option j < 32 of its mesh:
                        // {lo | hi << 16, g2*(L+1)}, the admissible split range of the
                        // current layer (dp_window) and the successor row
-  uint32_t *clist;     // [n_groups][ccap] (g << 16 | k0): chunks of up to kChunk
-                       // cells k0.. of state g inside the current layer's windows,
-                       // group-local compact order
+  uint32_t *clist;     // [n_groups][ccap] (g << 16 | k) of the cells inside the
+                       // current layer's windows, group-local compact order
   size_t ccap;         // L*G >= cells of any layer
   int32_t *gtot;       // [n_groups] window cells per group, reserved by
                        // dp_window's warps (zero between windowed layers)
@@ -149,7 +143,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], spanlen, winhi, wopt, clist, gtot, goff, ticket, gmeta, spart, H0,
+  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], spanlen, wopt, clist, gtot, goff, ticket, gmeta, spart, H0,
       H1, K0, K1, Hm0, Hm1, total;
 };
 
@@ -169,7 +163,6 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
     cur += align_up(ng * (t->G + 1) * sizeof(int2));
   }
   w.spanlen = cur; cur += align_up(ng * 2 * t->n_opts * 4);
-  w.winhi = cur; cur += align_up(ng * (t->G + 1) * 2);
   w.wopt = cur; cur += align_up(ng * (t->G + 1) * 32 * 8);
   w.clist = cur; cur += align_up(ng * (size_t)t->L * t->G * 4);
   w.gtot = cur; cur += align_up(ng * 4);
@@ -362,16 +355,14 @@ __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
   }
   klo = __reduce_min_sync(0xffffffffu, klo);
   khi = __reduce_max_sync(0xffffffffu, khi);
-  // chunks of up to kChunk consecutive k; winhi bounds the last chunk
-  const int n = khi >= klo ? (khi - klo + kChunk) / kChunk : 0;
+  const int n = khi >= klo ? khi - klo + 1 : 0;
   if (g <= G) {
     int base = 0;
     if (lane == 0 && n > 0) base = atomicAdd(b.gtot + group, n);
     base = __shfl_sync(0xffffffffu, base, 0);
     uint32_t *cl = b.clist + (size_t)group * b.ccap + base;
-    for (int t = lane; t < n; t += 32) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t * kChunk);
+    for (int t = lane; t < n; t += 32) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t);
     if (lane == 0) {
-      if (kChunk > 1) b.winhi[(size_t)group * (G + 1) + g] = (uint16_t)khi;
       b.irange[(s + 1) % 3][(size_t)group * (G + 1) + g] = make_int2(0x7fffffff, -1);
     }
   }
@@ -496,14 +487,15 @@ __device__ __forceinline__ void relax_entries(const int4 *__restrict__ st,
 // per chunk of cells of one (group, g) and reused by every cell of the chunk
 // (the opt_devs -> irange part of the per-cell dependent-load chain).
 struct OptLane {
-  int2 fr;    // finite-successor split range of g2 = g - devs (empty: not admissible)
+  int fr;     // lo | hi << 16: split range of the successor state g2 = g - devs
+              // whose entries are finite for some candidate (empty: lo > hi)
   int hbase;  // g2 * (L+1): successor row of g2
 };
 
 __device__ __forceinline__ OptLane opt_lane(const Batch &b, int s, int group, int g, int o,
                                             int avail, bool valid) {
   OptLane ol;
-  ol.fr = make_int2(1, 0);
+  ol.fr = 1;
   ol.hbase = 0;
   if (valid) {
     const int devs = __ldg(b.opt_devs + o), g2 = g - devs;
@@ -511,7 +503,9 @@ __device__ __forceinline__ OptLane opt_lane(const Batch &b, int s, int group, in
       // admissible splits: inside the range where state g2's successor entry
       // is finite for some candidate of the group (the rest are ones the
       // reference skips for all these candidates: fc == inf)
-      ol.fr = b.irange[(s - 1) % 3][(size_t)group * (b.G + 1) + g2];
+      const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (b.G + 1) + g2];
+      const int hi = min(b.L - s + 1, fr.y);
+      ol.fr = fr.x <= hi ? fr.x | (hi << 16) : 1;
       ol.hbase = g2 * (b.L + 1);
     }
   }
@@ -559,7 +553,6 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   unsigned cnt[CPL];  // #pool values <= t_max: tt <= t_max <=> prank < cnt
 #pragma unroll
   for (int c = 0; c < CPL; ++c) cnt[c] = (unsigned)b.tcnt[cand0 + c];
-  const int imax = L - s + 1;
   const size_t gbase = (size_t)group * b.hg;
   const double *Hg = b.H[(s - 1) & 1] + gbase * CW + lane * CPL;
   const uint16_t *Kg = b.K[(s - 1) & 1] + gbase * CW + lane * CPL;
@@ -582,7 +575,7 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     // lane j: admissible entries of option o's row (k) at this layer
     int len = 0, beg = 0;
     bool needkk = false;
-    const int lo_i = max(k, ol.fr.x), hi_i = min(imax, ol.fr.y);
+    const int lo_i = max(k, ol.fr & 0xffff), hi_i = (int)((unsigned)ol.fr >> 16);
     if (lane < nch && lo_i <= hi_i) {
       const int row = o * (L + 2) + k;
       // admissible splits also end at i <= L-s+1 (later successors are
@@ -887,11 +880,10 @@ __device__ __forceinline__ int find_group(const int32_t *__restrict__ goff, int 
 }
 
 // Windowed layers: only the cells inside dp_window's windows, enumerated
-// compactly as chunks of up to kChunk consecutive k of one (group, state g);
-// one warp per chunk over a grid capped at 256 warps per SM that strides
-// over the list -- no warp is spent on a provably infinite cell, and the
-// state's per-option data (opt_devs -> irange) is loaded once per chunk.
-// Finite-cell counts stay in registers while a warp's chunks stay in one
+// compactly, one warp per cell over a grid capped at 256 warps per SM that
+// strides over the list -- no warp is spent on a provably infinite cell, and
+// the state's per-option split ranges come precomputed from dp_window.
+// Finite-cell counts stay in shared memory while a warp's cells stay in one
 // group and go to one of kParts counter copies (dp_states_reduce sums them)
 // when it changes, so no warp waits at a block barrier for a slower one.
 template <int CPL>
@@ -933,26 +925,20 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
       cur = group;
     }
     const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
-    const int g = (int)(gk >> 16), k0 = (int)(gk & 0xffffu);
-    const int k1 = kChunk == 1 ? k0
-                               : min(k0 + kChunk - 1,
-                                     (int)__ldg(b.winhi + (size_t)group * (b.G + 1) + g));
+    const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
     const int4 gm = b.gmeta[g];
     // this layer's split ranges of the state's first 32 options (dp_window)
     OptLane ol0;
     {
       const int2 w = lane < gm.y ? __ldg(b.wopt + ((size_t)group * (b.G + 1) + g) * 32 + lane)
                                  : make_int2(1, 0);
-      ol0.fr = make_int2(w.x & 0xffff, (unsigned)w.x >> 16);
+      ol0.fr = w.x;
       ol0.hbase = w.y;
     }
-    for (int k = k0; k <= k1; ++k) {
-      int fin[CPL];
-      relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm.x, gm.y,
-                      ol0);
+    int fin[CPL];
+    relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm.x, gm.y, ol0);
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) cnt[c] += fin[c] ? 1u : 0u;
-    }
+    for (int c = 0; c < CPL; ++c) cnt[c] += fin[c] ? 1u : 0u;
   }
   if (cur >= 0) flush(cur);
 }
@@ -1169,7 +1155,6 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.cb_rows = 2 * t->n_meshes;
   for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);
   b.spanlen = (uint32_t *)(wb + w.spanlen);
-  b.winhi = (uint16_t *)(wb + w.winhi);
   b.wopt = (int2 *)(wb + w.wopt);
   b.clist = (uint32_t *)(wb + w.clist);
   b.ccap = (size_t)t->L * t->G;

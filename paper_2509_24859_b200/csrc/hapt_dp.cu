@@ -683,13 +683,15 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
         keep = keep && (lane == f || (lane < f ? lb <= bn : lb < bn));
         kept = __ballot_sync(0xffffffffu, keep);
       }
-      // kept entries first, in order; the rest of the stage is inert
+      // kept entries first, in order, padded with inert entries to a multiple
+      // of the transition loop's unroll
       const unsigned below = kept & ((1u << lane) - 1u);
       const int n = __popc(kept);
+      constexpr int U = Unroll<CPL>::value;
       if (keep) {
         stage_e[__popc(below)] = se;
         stage_k[__popc(below)] = sk;
-      } else {
+      } else if (n + (lane - __popc(below)) < (n + U - 1) / U * U) {
         stage_e[n + (lane - __popc(below))] = make_int4(0, 0, -1, 0);
         stage_k[n + (lane - __popc(below))] = 0;
       }

@@ -24,6 +24,12 @@ CONFIGS = {
          "64 microbatches",
     "D1": "Llama-2 70B proxy (2,006-op graph, 82 layers), 4 subclusters x 64 GPUs, "
           "100/50/25 Gbps, 128 microbatches",
+    "D2": "Llama-2 70B proxy (2,006-op graph, 164 layers), 4 subclusters x 64 GPUs, "
+          "100/50/25 Gbps, 128 microbatches",
+    "D3": "Llama-2 70B proxy (2,006-op graph, 246 layers), 4 subclusters x 64 GPUs, "
+          "100/50/25 Gbps, 128 microbatches",
+    "D4": "Llama-2 70B proxy blocks (2,000 ops, 320 layers: 2.26 M span-option cells), "
+          "4 subclusters x 64 GPUs, 100/50/25 Gbps, 128 microbatches",
     "E": "1F1B schedule-simulation sweep: synthetic plans x 128 microbatches, "
          "S in {2,3,4,6,8}, cross bandwidth log-uniform 1-200 Gbps",
 }

@@ -10,8 +10,8 @@ t_max candidate pool of the workload (config D1 by default: Llama-2 70B proxy,
 2,006-op graph clustered to 82 layers, 4 subclusters x 64 GPUs, B=128): the
 batched stage-partition DP over every candidate, the per-candidate Eq. 14
 scoring, and the global argmin (NCCL allreduce-argmin across ranks when
-N > 1).  The pool is strided across ranks, so total work is fixed as N grows
-("strong").
+N > 1).  The pool is dealt across ranks in contiguous blocks of 128
+candidates, so total work is fixed as N grows ("strong").
 
 value  : candidates/s with tables already resident in HBM (device timed,
          CUDA events on the launching stream, max over ranks).
@@ -455,7 +455,9 @@ def main():
     sw = tables.sweeper
     pool_all = np.asarray(store.feasible_t_values())
     P = len(pool_all)
-    mine = np.arange(rank, P, world)
+    # this rank's candidates: contiguous blocks of 128 dealt round-robin
+    # (distributed.PoolSharding.shard_positions)
+    mine = sharding.shard_positions(P) if sharding is not None else np.arange(P)
     tmax = torch.from_numpy(pool_all[mine]).to(device)
     gidx = torch.from_numpy(mine.astype(np.int64)).to(device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
@@ -489,8 +491,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     dev_s = sum(s.elapsed_time(e) for s, e in zip(s_ev, e_ev)) * 1e-3
+    rank_ms = [dev_s / args.steps * 1e3]
     t = torch.tensor([dev_s], dtype=torch.float64, device=device)
     if world > 1:
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        rank_ms = [float(x.item()) / args.steps * 1e3 for x in parts]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_s = float(t.item())
     value = P * args.steps / dev_s
@@ -557,6 +563,7 @@ def main():
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
+        "rank_ms_per_step": rank_ms,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,

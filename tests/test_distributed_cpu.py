@@ -70,7 +70,7 @@ def _worker(rank, world, port, name, out_q, min_shard):
         feas = [i for i in surv if ev.best_s[i] >= 0]
         best = min(feas, key=lambda i: (ev.tstar[i], pool[i]))
         # allreduce-argmin over a rank-local shard of the whole pool
-        mine = list(range(rank, len(pool), world))
+        mine = [int(i) for i in sh.shard_positions(len(pool))]
         res = sw.evaluate([pool[i] for i in mine], B)
         w = res.winner
         g_t, g_i = sh.allreduce_argmin(float(res.tstar[w]) if w >= 0 else float("inf"),

@@ -76,7 +76,9 @@ int cpl_for(const hapt_tables *t, int n_cand) {
   // ~1,000 candidates, or with too few warps per layer, CPL = 2 stays ahead)
   const long cells = (long)t->L * t->G;
   const long warps4 = cells * ((n_cand + 127) / 128);
-  if (n_cand >= 1024 && warps4 >= 80000) return 4;
+  // (v18, tools/gpu/cpl.py: C's 1,688 candidates on 102 x 64 cells run
+  // faster at 2, D1's 1,786 on 82 x 256 cells at 4)
+  if (n_cand >= 1024 && warps4 >= 150000) return 4;
   const long warps2 = cells * ((n_cand + 63) / 64);
   return (warps2 >= 16384 && n_cand > 240) ? 2 : 1;
 }

@@ -2,9 +2,9 @@
 
 Every t_max candidate's DP is independent (planner.py:526-531),
 so a batch of candidates is dealt across ranks in contiguous blocks of 128
-candidates, round-robin (block b goes to rank b mod W): blocks keep the DP's
-candidate groups t_max-contiguous (tight lane bounds), and dealing them
-round-robin balances the ranks as the activated span count grows with t_max.
+candidates, back and forth (0..W-1, W-1..0, ...): blocks keep the DP's
+candidate groups t_max-contiguous (tight lane bounds), and the boustrophedon
+deal balances the ranks as the activated span count grows with t_max.
 Each rank builds the same K1 tables locally (microseconds; cheaper than a
 broadcast).  The only exchange steps are
 
@@ -58,15 +58,22 @@ class PoolSharding:
         neighbouring t_max, so a DP candidate group (32-128 lanes) keeps tight
         lane bounds and finite ranges (a strided share spreads each group
         over a W-times wider t_max range: D3 at 4 GPUs ran 3.1x instead of
-        ~4x); dealing the blocks round-robin keeps the ranks balanced as
+        ~4x); dealing the blocks back and forth keeps the ranks balanced as
         the per-candidate work grows with t_max."""
         return self._positions(n, self.rank)
 
     def _positions(self, n: int, rank: int) -> np.ndarray:
-        # blocks of BLOCK, smaller when n < BLOCK * world so every rank works
-        blk = max(1, min(self.BLOCK, -(-n // self.world)))
+        # at most BLOCK per block, and a multiple of world blocks so every
+        # rank gets the same number (D1's 1,786 at 4 GPUs: 16 blocks of 112)
+        W = self.world
+        nblk = W * max(1, -(-n // (W * self.BLOCK)))
+        blk = max(1, -(-n // nblk))
         pos = np.arange(n)
-        return pos[(pos // blk) % self.world == rank]
+        b = pos // blk
+        # boustrophedon deal (0..W-1, W-1..0, ...): work grows with t_max, so a
+        # plain round-robin would always hand the last rank the larger block
+        owner = np.where((b // W) % 2 == 0, b % W, W - 1 - b % W)
+        return pos[owner == rank]
 
     def shard(self, indices):
         idx = list(indices)

@@ -12,7 +12,7 @@ from helpers import assert_plan_equal, build, expected, load_json, plan_dict, se
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["A", "B", "C", "D1", "D2", "D3"])
+@pytest.mark.parametrize("name", ["A", "B", "C", "D1", "D2", "D3", "D4"])
 def test_search_configs_equal_reference(name):
     from paper_2509_24859_b200.planner import search, validate_plan
 

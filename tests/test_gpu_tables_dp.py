@@ -21,8 +21,10 @@ def sha(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("name", ["A", "B", "C", "D1", "D2", "D3"])
+@pytest.mark.parametrize("name", ["A", "B", "C", "D1", "D2", "D3", "D4"])
 def test_device_tables_equal_reference(name):
+    """(D4: 320 layers, n_opts * L(L+1)/2 = 2.26 M span-option cells, past
+    the 2^21 packing limit of round 1.)"""
     """hapt_tables_build reproduces DpTables + the t_max pool + StoreStats."""
     from paper_2509_24859_b200.planner import DpTables
 

@@ -30,9 +30,10 @@ def main():
     pool = np.asarray(store.feasible_t_values())
     sw = tables.sweeper
     for W in [int(w) for w in args.worlds.split(",")]:
-        blk = max(1, min(128, -(-len(pool) // W)))
-        pos = np.arange(len(pool))
-        mine = pool[(pos // blk) % W == 0]
+        blk = max(1, -(-len(pool) // (W * max(1, -(-len(pool) // (W * 128))))))
+        b = np.arange(len(pool)) // blk
+        owner = np.where((b // W) % 2 == 0, b % W, W - 1 - b % W)
+        mine = pool[owner == W - 1]  # the rank with the heaviest first block
         tm = torch.from_numpy(mine).cuda()
         row = []
         for c in args.cpl.split(","):

@@ -63,11 +63,12 @@ class PoolSharding:
         return self._positions(n, self.rank)
 
     def _positions(self, n: int, rank: int) -> np.ndarray:
-        # at most BLOCK per block, and a multiple of world blocks so every
-        # rank gets the same number (D1's 1,786 at 4 GPUs: 16 blocks of 112)
+        # blocks aligned to the DP's candidate groups: 128 when a rank's share
+        # runs at 4 candidates per lane (>= 1,024 candidates), else 64 (finer
+        # deal: D1's 1,786 at 4 GPUs = 28 blocks, 7 per rank); a group never
+        # straddles two blocks, which would put a t_max gap inside it
         W = self.world
-        nblk = W * max(1, -(-n // (W * self.BLOCK)))
-        blk = max(1, -(-n // nblk))
+        blk = self.BLOCK if n >= 1024 * W else self.BLOCK // 2
         pos = np.arange(n)
         b = pos // blk
         # boustrophedon deal (0..W-1, W-1..0, ...): work grows with t_max, so a

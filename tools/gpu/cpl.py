@@ -30,7 +30,7 @@ def main():
     pool = np.asarray(store.feasible_t_values())
     sw = tables.sweeper
     for W in [int(w) for w in args.worlds.split(",")]:
-        blk = max(1, -(-len(pool) // (W * max(1, -(-len(pool) // (W * 128))))))
+        blk = 128 if len(pool) >= 1024 * W else 64
         b = np.arange(len(pool)) // blk
         owner = np.where((b // W) % 2 == 0, b % W, W - 1 - b % W)
         mine = pool[owner == W - 1]  # the rank with the heaviest first block

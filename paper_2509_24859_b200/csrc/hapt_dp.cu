@@ -42,9 +42,6 @@ __device__ unsigned long long g_work[8];  // executed / admissible / improving l
 #endif
 constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
-#ifndef HAPT_CONTIG
-#define HAPT_CONTIG 0  // 1: relax blocks take contiguous slices of the cell list
-#endif
 #ifndef HAPT_WIN_MINLEN
 #define HAPT_WIN_MINLEN 1  // window hull also bounded by each option's shortest span
 #endif  // window cells of one (group, state) per relax warp
@@ -925,15 +922,7 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
 #pragma unroll
     for (int c = 0; c < CPL; ++c) cnt[c] = 0u;
   };
-#if HAPT_CONTIG
-  // each block walks one contiguous slice of the list (neighbouring cells of
-  // the same states read the same successor rows: L1 reuse)
-  const int per = (total + gridDim.x - 1) / gridDim.x;
-  const int i_end = min(total, (blockIdx.x + 1) * per);
-  for (int idx = blockIdx.x * per + warp; idx < i_end; idx += kWarps) {
-#else
   for (int idx = blockIdx.x * kWarps + warp; idx < total; idx += gridDim.x * kWarps) {
-#endif
     const int group = find_group(b.goff, b.n_groups, idx, lane);
     if (group != cur) {
       if (cur >= 0) flush(cur);

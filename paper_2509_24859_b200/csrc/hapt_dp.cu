@@ -34,6 +34,9 @@ namespace hapt {
 namespace {
 
 #ifdef HAPT_COUNT_WORK
+__device__ unsigned long long g_layer[4096 * 8];  // per layer: tasks, empty, chunks,
+                                                  // staged, kept by bound, kept after probe,
+                                                  // finite cells
 __device__ unsigned long long g_work[8];  // executed / admissible / improving lane-transitions,
                                           // -, cell-tasks, empty cells, all-infinite cells, staged chunks
 #endif
@@ -609,6 +612,10 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       atomicAdd(&g_work[4], 1ull);
       if (T == 0 && nopt <= 32) atomicAdd(&g_work[5], 1ull);
       atomicAdd(&g_work[7], (unsigned long long)((T + 31) / 32));
+      atomicAdd(&g_layer[s * 8 + 0], 1ull);
+      if (T == 0) atomicAdd(&g_layer[s * 8 + 1], 1ull);
+      atomicAdd(&g_layer[s * 8 + 2], (unsigned long long)((T + 31) / 32));
+      atomicAdd(&g_layer[s * 8 + 3], (unsigned long long)T);
     }
 #endif
     const bool anykk = __any_sync(0xffffffffu, needkk);
@@ -660,6 +667,9 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       // lb > bn, is never the first minimum and is dropped; f itself stays
       // and is relaxed in its own place, so the scan order is the reference's.
       unsigned kept = __ballot_sync(0xffffffffu, keep);
+#ifdef HAPT_COUNT_WORK
+      if (lane == 0) atomicAdd(&g_layer[s * 8 + 4], (unsigned long long)__popc(kept));
+#endif
       if (b.probe && __popc(kept) > HAPT_PROBE_MIN) {
         const unsigned lh = keep ? (unsigned)__double2hiint(lb) : 0xffffffffu;
         const unsigned ml = __reduce_min_sync(0xffffffffu, lh);
@@ -689,6 +699,9 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       // of the transition loop's unroll
       const unsigned below = kept & ((1u << lane) - 1u);
       const int n = __popc(kept);
+#ifdef HAPT_COUNT_WORK
+      if (lane == 0) atomicAdd(&g_layer[s * 8 + 5], (unsigned long long)n);
+#endif
       constexpr int U = Unroll<CPL>::value;
       if (keep) {
         stage_e[__popc(below)] = se;
@@ -802,6 +815,9 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
   hh = __reduce_min_sync(0xffffffffu, hh);
   if (lane == 0) b.Hmin[s & 1][hm_idx] = __hiloint2double((int)hh, 0);
   const bool wfin = __any_sync(0xffffffffu, anyfin);
+#ifdef HAPT_COUNT_WORK
+  if (lane == 0 && wfin) atomicAdd(&g_layer[s * 8 + 6], 1ull);
+#endif
   if (wfin) {  // otherwise Hmin = +inf already shields the slots (see above)
     double *ho = b.H[s & 1] + o_idx;
     uint16_t *ko = b.K[s & 1] + o_idx;
@@ -1449,6 +1465,13 @@ extern "C" int hapt_activated_pairs(const hapt_tables *t, const double *tmax, in
 }
 
 #ifdef HAPT_COUNT_WORK
+extern "C" int hapt_debug_layers(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, hapt::g_layer, sizeof(unsigned long long) * 4096 * 8) ==
+                 cudaSuccess
+             ? HAPT_OK
+             : HAPT_ECUDA;
+}
 // instrumented build only: cumulative transition counters of the DP loop
 extern "C" int hapt_debug_work(unsigned long long *out) {
   cudaDeviceSynchronize();

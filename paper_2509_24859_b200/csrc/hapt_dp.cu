@@ -112,8 +112,10 @@ struct Batch {
   const double *tmax;  // [n_cand]
   double *tmax_pad;    // [n_groups*cw]
   int32_t *tcnt;       // [n_groups*cw]  #pool values <= t_max
-  uint16_t *cut_sr;    // [n_groups][rows] entries of a row before its suffix-min
-                       // pool rank reaches the group's largest bound
+  uint2 *rowmeta;      // [n_groups][rows] {span_off of the row, cut | kmin << 16}:
+                       // cut = entries of the row before its suffix-min pool rank
+                       // reaches the group's largest bound, kmin = row_kmin (one
+                       // 8-byte load per option in the cell prologue)
   uint8_t *kc;         // [n_groups][2*n_meshes][L+1][cw] ceil(2c/t_max)+1 of every
                        // boundary row entry, 0xFF where c > t_max (_dp.pyx:76-82)
   int cb_rows;         // 2*n_meshes
@@ -148,7 +150,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, cut_sr, kc, ir[3], spanlen, wopt, clist, gtot, goff, ticket, gmeta, spart, H0,
+  size_t tmax_pad, tcnt, rowmeta, kc, ir[3], spanlen, wopt, clist, gtot, goff, ticket, gmeta, spart, H0,
       H1, K0, K1, Hm0, Hm1, total;
 };
 
@@ -161,7 +163,7 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   size_t cur = 0;
   w.tmax_pad = cur; cur += align_up(np * 8);
   w.tcnt = cur; cur += align_up(np * 4);
-  w.cut_sr = cur; cur += align_up(ng * rows * 2);
+  w.rowmeta = cur; cur += align_up(ng * rows * 8);
   w.kc = cur; cur += align_up(ng * 2 * t->n_meshes * (t->L + 1) * cw);
   for (int j = 0; j < 3; ++j) {
     w.ir[j] = cur;
@@ -257,7 +259,8 @@ __global__ void dp_prep(Batch b) {
       const int mid = (lo + hi) >> 1;
       if (b.span_srank[mid] < gm) lo = mid + 1; else hi = mid;
     }
-    b.cut_sr[(size_t)group * b.rows + row] = (uint16_t)(lo - beg);
+    b.rowmeta[(size_t)group * b.rows + row] =
+        make_uint2((unsigned)beg, (unsigned)(lo - beg) | ((unsigned)b.row_kmin[row] << 16));
     if (lo > beg) {
       const int o = row / (b.L + 2), k = row - o * (b.L + 2);
       atomicMax(b.spanlen + ((size_t)group * 2 + 0) * b.n_opts + o,
@@ -585,9 +588,8 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       const int row = o * (L + 2) + k;
       // admissible splits also end at i <= L-s+1 (later successors are
       // provably infinite) and before the group's suffix-rank cut
-      const int cut = __ldg(b.cut_sr + (size_t)group * b.rows + row);
-      const int soff = __ldg(b.span_off + row);
-      const int kmin = __ldg(b.row_kmin + row);
+      const uint2 rm = __ldg(b.rowmeta + (size_t)group * b.rows + row);
+      const int soff = (int)rm.x, cut = (int)(rm.y & 0xffffu), kmin = (int)(rm.y >> 16);
       const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
       const int a = __ldg(pos + lo_i - 1);
       const int z = min((int)__ldg(pos + hi_i), cut);
@@ -1170,7 +1172,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.tmax = tmax;
   b.tmax_pad = (double *)(wb + w.tmax_pad);
   b.tcnt = (int32_t *)(wb + w.tcnt);
-  b.cut_sr = (uint16_t *)(wb + w.cut_sr);
+  b.rowmeta = (uint2 *)(wb + w.rowmeta);
   b.kc = (uint8_t *)(wb + w.kc);
   b.cb_rows = 2 * t->n_meshes;
   for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);

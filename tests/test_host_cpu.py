@@ -160,3 +160,26 @@ def test_dag_structure_lazy_edges():
     assert dag.node_name(f) == "F[1,1]"
     with pytest.raises(SimulationError):
         build_dag([1.0], [1.0], [0.1], build_program(classic_counts(1), 2))
+
+
+@pytest.mark.parametrize("n,W", [(1786, 2), (1786, 4), (15925, 4), (124, 2), (7019, 8)])
+def test_pool_deal_blocks(n, W):
+    """PoolSharding's deal: every candidate on exactly one rank, in contiguous
+    group-aligned blocks (64 or 128), equal block counts +-1."""
+    import numpy as np
+
+    from paper_2509_24859_b200.distributed import PoolSharding
+
+    sh = object.__new__(PoolSharding)
+    sh.world = W
+    parts = [sh._positions(n, r) for r in range(W)]
+    allp = np.sort(np.concatenate(parts))
+    assert np.array_equal(allp, np.arange(n))
+    blk = 128 if n >= 1024 * W else 64
+    for p in parts:
+        blocks = set(int(x) // blk for x in p)
+        for b in blocks:  # whole blocks only
+            lo, hi = b * blk, min(n, (b + 1) * blk)
+            assert np.isin(np.arange(lo, hi), p).all()
+    counts = [len(set(int(x) // blk for x in p)) for p in parts]
+    assert max(counts) - min(counts) <= 1

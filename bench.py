@@ -455,11 +455,9 @@ def main():
     sw = tables.sweeper
     pool_all = np.asarray(store.feasible_t_values())
     P = len(pool_all)
-    # this rank's candidates: contiguous blocks of 64 / 128, heaviest first to
-    # the least-loaded rank by activated span count
+    # this rank's candidates: contiguous blocks of 128 dealt round-robin
     # (distributed.PoolSharding.shard_positions)
-    mine = (sharding.shard_positions(P, sw.activated(pool_all)) if sharding is not None
-            else np.arange(P))
+    mine = sharding.shard_positions(P) if sharding is not None else np.arange(P)
     tmax = torch.from_numpy(pool_all[mine]).to(device)
     gidx = torch.from_numpy(mine.astype(np.int64)).to(device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)

@@ -52,20 +52,17 @@ class PoolSharding:
 
     BLOCK = 128  # candidates per contiguous block (the widest DP candidate group)
 
-    def shard_positions(self, n: int, weights=None) -> np.ndarray:
+    def shard_positions(self, n: int) -> np.ndarray:
         """Positions of this rank's share of n sorted candidates: contiguous
-        blocks of BLOCK candidates.  Candidates of a block have neighbouring
-        t_max, so a DP candidate group (32-128 lanes) keeps tight lane bounds
-        and finite ranges (a strided share spreads each group over a W-times
-        wider t_max range: D3 at 4 GPUs ran 3.1x instead of ~4x).  With
-        per-candidate `weights` (the activated span count, a work estimate:
-        Sweeper.activated) blocks go heaviest first to the least-loaded rank;
-        without, they are dealt back and forth (0..W-1, W-1..0, ...), since
-        work grows with t_max.  Deterministic, so every rank computes every
-        rank's share."""
-        return self._positions(n, self.rank, weights)
+        blocks of BLOCK dealt round-robin.  Candidates of a block have
+        neighbouring t_max, so a DP candidate group (32-128 lanes) keeps tight
+        lane bounds and finite ranges (a strided share spreads each group
+        over a W-times wider t_max range: D3 at 4 GPUs ran 3.1x instead of
+        ~4x); dealing the blocks back and forth keeps the ranks balanced as
+        the per-candidate work grows with t_max."""
+        return self._positions(n, self.rank)
 
-    def _positions(self, n: int, rank: int, weights=None) -> np.ndarray:
+    def _positions(self, n: int, rank: int) -> np.ndarray:
         # blocks aligned to the DP's candidate groups: 128 when a rank's share
         # runs at 4 candidates per lane (>= 1,024 candidates), else 64 (finer
         # deal: D1's 1,786 at 4 GPUs = 28 blocks, 7 per rank); a group never
@@ -74,23 +71,14 @@ class PoolSharding:
         blk = self.BLOCK if n >= 1024 * W else self.BLOCK // 2
         pos = np.arange(n)
         b = pos // blk
-        nb = int(b[-1]) + 1 if n else 0
-        if weights is None:
-            owner_b = np.arange(nb)
-            owner_b = np.where((owner_b // W) % 2 == 0, owner_b % W, W - 1 - owner_b % W)
-        else:
-            wb = np.bincount(b, weights=np.asarray(weights, dtype=np.float64), minlength=nb)
-            load = np.zeros(W)
-            owner_b = np.empty(nb, dtype=np.int64)
-            for j in sorted(range(nb), key=lambda j: (-wb[j], j)):  # LPT, ties by index
-                r = int(np.argmin(load))
-                owner_b[j] = r
-                load[r] += wb[j]
-        return pos[owner_b[b] == rank]
+        # boustrophedon deal (0..W-1, W-1..0, ...): work grows with t_max, so a
+        # plain round-robin would always hand the last rank the larger block
+        owner = np.where((b // W) % 2 == 0, b % W, W - 1 - b % W)
+        return pos[owner == rank]
 
-    def shard(self, indices, weights=None):
+    def shard(self, indices):
         idx = list(indices)
-        return [idx[p] for p in self.shard_positions(len(idx), weights)]
+        return [idx[p] for p in self.shard_positions(len(idx))]
 
     def _all_gather(self, local: torch.Tensor, width: int) -> torch.Tensor:
         """Gather equally padded [width, ...] tensors from every rank."""
@@ -107,9 +95,8 @@ class PoolSharding:
         rank returns the full (tstar, best_s, states) in `todo` order, plus
         F[s,1,G] per candidate when want_ftop (search_batches)."""
         todo = list(todo)
-        wts = sweeper.activated(pool[todo]) if len(todo) >= 1024 else None
-        mine = self.shard(todo, wts)
-        width = max(len(self._positions(len(todo), r, wts)) for r in range(self.world))
+        mine = self.shard(todo)
+        width = max(len(self._positions(len(todo), r)) for r in range(self.world))
         s1 = sweeper.tables.s_max + 1 if want_ftop else 0
         cols = 3 + s1
         if mine:
@@ -128,7 +115,7 @@ class PoolSharding:
         states = np.empty(len(todo), dtype=np.int64)
         ftop = np.empty((len(todo), s1)) if want_ftop else None
         for r in range(self.world):
-            pos = self._positions(len(todo), r, wts)
+            pos = self._positions(len(todo), r)
             blk = allv[r, : len(pos)]
             tstar[pos] = blk[:, 0].view(np.float64)
             best_s[pos] = blk[:, 1]

@@ -33,9 +33,8 @@ def main():
         sh = object.__new__(PoolSharding)
         sh.world = W
         row = []
-        wts = sw.activated(pool) if os.environ.get("WEIGHTED", "1") == "1" else None
         for r in range(W):
-            mine = pool[sh._positions(len(pool), r, wts)]
+            mine = pool[sh._positions(len(pool), r)]
             tm = torch.from_numpy(mine).cuda()
             for _ in range(2):
                 sw.sweep_device(tm)

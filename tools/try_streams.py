@@ -34,8 +34,10 @@ def main():
     n = pool.numel()
     s1 = t.s_max + 1
     for k in (1, 2, 3, 4):
-        # strided split: every part gets the same mix of small and large t_max
-        parts = [torch.arange(j, n, k, device="cuda") for j in range(k)]
+        # contiguous 128-candidate blocks dealt back and forth (as across GPUs)
+        b = np.arange(n) // 128
+        owner = np.where((b // k) % 2 == 0, b % k, k - 1 - b % k)
+        parts = [torch.from_numpy(np.flatnonzero(owner == j)).cuda() for j in range(k)]
         tm = [pool[p].contiguous() for p in parts]
         streams = [torch.cuda.Stream() for _ in range(k)]
         ws = [torch.empty(lib.hapt_dp_workspace_bytes(ctypes.byref(t.t), x.numel()),

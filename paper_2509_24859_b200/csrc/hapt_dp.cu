@@ -689,7 +689,8 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           double m = bv[c];
-          if (pz < cnt[c] && (!anykk || kp[c] <= pk)) m = fmin(m, __dadd_rn(pt, hp[c]));
+          const double v = __dadd_rn(pt, hp[c]);  // never NaN: tt, H >= 0 (or +inf)
+          if (pz < cnt[c] && (!anykk || kp[c] <= pk) && v < m) m = v;
           mh = max(mh, (unsigned)__double2hiint(m));
         }
         mh = __reduce_max_sync(0xffffffffu, mh);

@@ -154,9 +154,9 @@ struct WsLayout {
       H1, K0, K1, Hm0, Hm1, total;
 };
 
-WsLayout ws_layout(const hapt_tables *t, int n_cand) {
+WsLayout ws_layout(const hapt_tables *t, int n_cand, int cpl) {
   WsLayout w{};
-  const size_t cw = 32 * (size_t)cpl_for(t, n_cand);
+  const size_t cw = 32 * (size_t)cpl;
   const size_t ng = (n_cand + cw - 1) / cw, np = ng * cw;
   const size_t hg = (size_t)(t->G + 1) * (t->L + 1);
   const size_t rows = (size_t)t->n_opts * (t->L + 2);
@@ -185,6 +185,49 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   w.Hm1 = cur; cur += align_up(ng * hg * 8);
   w.total = cur;
   return w;
+}
+
+WsLayout ws_layout(const hapt_tables *t, int n_cand) {
+  return ws_layout(t, n_cand, cpl_for(t, n_cand));
+}
+
+// Large batches run as two independent halves of whole candidate groups on
+// two side streams, so one half's per-layer tails and window passes overlap
+// the other's work (measured, tools/try_streams.py at 4 candidates per lane:
+// D1 5.14 -> 5.01 ms, D2 78.8 -> 75.3 ms).  Both halves keep the full
+// batch's candidates-per-lane.  Off when full outputs are requested.
+// Large batches run as two independent halves (whole candidate groups, the
+// low-t_max half and the high-t_max half) on two side streams, so one
+// half's per-layer window passes and tails overlap the other's work.  Both
+// halves keep the full batch's candidates per lane.  Measured (profiles/r2,
+// tools/gpu/envs.sh HAPT_SPLIT=0): D2 78.2 -> 73.6 ms, D3 506 -> 472 ms;
+// D1 (14 groups) and smaller batches are faster unsplit (5.15 vs 5.52 ms),
+// alternating groups between the halves measured worse than contiguous
+// halves (D2 74.6, D3 481, D1 5.29 ms).  Off when full outputs are requested.
+struct Split {
+  int parts, cpl;
+  int n[2];
+  size_t ws[2];  // aligned workspace bytes of each part
+};
+
+Split split_plan(const hapt_tables *t, int n_cand, bool full) {
+  Split sp{};
+  sp.cpl = cpl_for(t, n_cand);
+  const int cw = 32 * sp.cpl, ng = (n_cand + cw - 1) / cw;
+  static const bool on = [] {
+    const char *e = getenv("HAPT_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  if (on && !full && sp.cpl == 4 && ng >= 24) {
+    sp.parts = 2;
+    sp.n[0] = (ng / 2) * cw;
+    sp.n[1] = n_cand - sp.n[0];
+  } else {
+    sp.parts = 1;
+    sp.n[0] = n_cand;
+  }
+  for (int j = 0; j < sp.parts; ++j) sp.ws[j] = align_up(ws_layout(t, sp.n[j], sp.cpl).total);
+  return sp;
 }
 
 __device__ __forceinline__ int upper_bound(const double *a, int n, double v) {
@@ -1140,8 +1183,9 @@ __global__ void k_activated(const double *pool, const int64_t *counters,
 }
 
 Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *ftop,
-                 int64_t *states, const hapt_dp_full *full, void *work) {
-  WsLayout w = ws_layout(t, n_cand);
+                 int64_t *states, const hapt_dp_full *full, void *work, int cpl = 0) {
+  if (cpl == 0) cpl = cpl_for(t, n_cand);
+  WsLayout w = ws_layout(t, n_cand, cpl);
   char *wb = (char *)work;
   Batch b{};
   b.spans = t->spans;
@@ -1162,7 +1206,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.G = t->G;
   b.s_max = t->s_max;
   b.n_cand = n_cand;
-  b.cpl = cpl_for(t, n_cand);
+  b.cpl = cpl;
   {
     static const int probe = getenv("HAPT_PROBE") ? atoi(getenv("HAPT_PROBE")) : 1;
     b.probe = probe;
@@ -1285,8 +1329,34 @@ using namespace hapt;
 
 extern "C" size_t hapt_dp_workspace_bytes(const hapt_tables *t, int32_t n_cand) {
   if (!t || n_cand < 1) return 0;
-  return ws_layout(t, n_cand).total;
+  const Split sp = split_plan(t, n_cand, false);
+  size_t total = 0;
+  for (int j = 0; j < sp.parts; ++j) total += sp.ws[j];
+  return max(total, align_up(ws_layout(t, n_cand).total));  // (full outputs: one part)
 }
+
+namespace {
+// side streams of the calling host thread on the current device (fork/join
+// of a split sweep; the caller's stream orders everything around them)
+struct SideStreams {
+  int dev = -1;
+  cudaStream_t s[2] = {nullptr, nullptr};
+};
+thread_local SideStreams t_side;
+
+int side_streams(cudaStream_t (&out)[2]) {
+  int dev = 0;
+  HAPT_CUDA(cudaGetDevice(&dev));
+  if (t_side.dev != dev) {
+    for (int j = 0; j < 2; ++j)
+      HAPT_CUDA(cudaStreamCreateWithFlags(&t_side.s[j], cudaStreamNonBlocking));
+    t_side.dev = dev;  // (streams of a previous device stay alive: rare)
+  }
+  out[0] = t_side.s[0];
+  out[1] = t_side.s[1];
+  return HAPT_OK;
+}
+}  // namespace
 
 extern "C" int hapt_dp_sweep_batch(const hapt_tables *t, const double *tmax, int32_t n_cand,
                                    double *ftop, int64_t *states, const hapt_dp_full *full,
@@ -1300,12 +1370,42 @@ extern "C" int hapt_dp_sweep_batch(const hapt_tables *t, const double *tmax, int
     set_error("hapt_dp_sweep_batch: F/N need bp_i and bp_o, which go together");
     return HAPT_EINVAL;
   }
-  if (work_bytes < ws_layout(t, n_cand).total) {
-    set_error("hapt_dp_sweep_batch: workspace %zu < %zu", work_bytes, ws_layout(t, n_cand).total);
+  const Split sp = split_plan(t, n_cand, full != nullptr);
+  size_t need = 0;
+  for (int j = 0; j < sp.parts; ++j) need += sp.ws[j];
+  if (work_bytes < need) {
+    set_error("hapt_dp_sweep_batch: workspace %zu < %zu", work_bytes, need);
     return HAPT_ENOSPACE;
   }
-  Batch b = make_batch(t, tmax, n_cand, ftop, states, full, work);
-  return run_sweep(b, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (sp.parts == 1) {
+    Batch b = make_batch(t, tmax, n_cand, ftop, states, full, work, sp.cpl);
+    return run_sweep(b, st);
+  }
+  cudaStream_t side[2];
+  if (const int rc = side_streams(side)) return rc;
+  cudaEvent_t fork, done[2];
+  HAPT_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  HAPT_CUDA(cudaEventRecord(fork, st));
+  char *w = (char *)work;
+  int off = 0;
+  for (int j = 0; j < 2; ++j) {
+    HAPT_CUDA(cudaStreamWaitEvent(side[j], fork, 0));
+    Batch b = make_batch(t, tmax + off, sp.n[j], ftop + (size_t)off * (t->s_max + 1),
+                         states + off, nullptr, w, sp.cpl);
+    const int rc = run_sweep(b, side[j]);
+    if (rc != HAPT_OK) return rc;
+    HAPT_CUDA(cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming));
+    HAPT_CUDA(cudaEventRecord(done[j], side[j]));
+    HAPT_CUDA(cudaStreamWaitEvent(st, done[j], 0));
+    w += sp.ws[j];
+    off += sp.n[j];
+  }
+  // events are released once the work they mark has completed
+  cudaEventDestroy(fork);
+  cudaEventDestroy(done[0]);
+  cudaEventDestroy(done[1]);
+  return HAPT_OK;
 }
 
 extern "C" int hapt_dp_select(const double *ftop, const double *tmax, int32_t n_cand,

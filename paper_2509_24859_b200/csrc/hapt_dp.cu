@@ -78,9 +78,14 @@ int cpl_for(const hapt_tables *t, int n_cand) {
   const long warps4 = cells * ((n_cand + 127) / 128);
   // (v18, tools/gpu/cpl.py: C's 1,688 candidates on 102 x 64 cells run
   // faster at 2, D1's 1,786 on 82 x 256 cells at 4)
-  if (n_cand >= 1024 && warps4 >= 150000) return 4;
+  // (round 2, tools/gpu/cpl_sizes.py on D1 / C / D2 slices: two per lane win
+  // from ~40 candidates once a layer has a few thousand cell-warps, e.g. D1
+  // 38: 1.08 -> 0.89 ms, 192: 1.82 -> 1.72 ms, C 38: 0.265 -> 0.231 ms, D2 128:
+  // 5.06 -> 3.69 ms; four win on D2 from 890 candidates (15.6 -> 11.5 ms) but
+  // not on D1 at 890 (3.22 vs 3.60 ms); config B's small tables stay at one)
+  if (warps4 >= 150000) return 4;
   const long warps2 = cells * ((n_cand + 63) / 64);
-  return (warps2 >= 16384 && n_cand > 240) ? 2 : 1;
+  return (warps2 >= 4096 && n_cand > 32) ? 2 : 1;
 }
 
 #ifndef HAPT_U4
@@ -130,11 +135,14 @@ struct Batch {
   uint32_t *clist;     // [n_groups][ccap] (g << 16 | k) of the cells inside the
                        // current layer's windows, group-local compact order
   size_t ccap;         // L*G >= cells of any layer
-  int32_t *gtot;       // [n_groups] window cells per group, reserved by
-                       // dp_window's warps (zero between windowed layers)
-  int32_t *goff;       // [n_groups+1] exclusive prefix of gtot: the compact cell
-                       // index space dp_relax_compact walks
-  unsigned *ticket;    // dp_window's last-block counter (self-resetting)
+  int32_t *gtot[2];    // [n_groups] window cells per group at layers of each
+                       // parity, reserved by dp_window's warps; dp_window(s)
+                       // zeroes the other parity's (last read by dp_relax(s-1));
+                       // dp_relax_compact turns them into the compact cell
+                       // index space it walks (a prefix in shared memory)
+  int2 *gopt;          // [G+1][32] per state g and option j < 32 of its mesh:
+                       // {o, g - devs_o} ({-1, -1} past the mesh's options, g2 = -1
+                       // where devs_o exceeds the state's available devices)
   int4 *gmeta;         // [G+1] per state g: first option of its mesh, option count,
                        // available devices, successor boundary row (g_crow)
   uint32_t *spart;     // [kParts][n_groups*cw] finite-cell counts of windowed
@@ -150,7 +158,7 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, rowmeta, kc, ir[3], spanlen, wopt, clist, gtot, goff, ticket, gmeta, spart, H0,
+  size_t tmax_pad, tcnt, rowmeta, kc, ir[3], spanlen, wopt, clist, gtot[2], gopt, gmeta, spart, H0,
       H1, K0, K1, Hm0, Hm1, total;
 };
 
@@ -172,9 +180,9 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand, int cpl) {
   w.spanlen = cur; cur += align_up(ng * 2 * t->n_opts * 4);
   w.wopt = cur; cur += align_up(ng * (t->G + 1) * 32 * 8);
   w.clist = cur; cur += align_up(ng * (size_t)t->L * t->G * 4);
-  w.gtot = cur; cur += align_up(ng * 4);
-  w.goff = cur; cur += align_up((ng + 1) * 4);
-  w.ticket = cur; cur += align_up(4);
+  w.gtot[0] = cur; cur += align_up(ng * 4);
+  w.gtot[1] = cur; cur += align_up(ng * 4);
+  w.gopt = cur; cur += align_up((size_t)(t->G + 1) * 32 * sizeof(int2));
   w.gmeta = cur; cur += align_up((t->G + 1) * sizeof(int4));
   w.spart = cur; cur += align_up(kParts * np * 4);
   w.H0 = cur; cur += align_up(ng * hg * cw * 8);
@@ -263,8 +271,10 @@ __global__ void dp_prep(Batch b) {
     atomicMax(&s_gmax, cnt);
   }
   if (part == 0) {
-    if (group == 0 && threadIdx.x == 0) *b.ticket = 0u;
-    if (threadIdx.x == 0) b.gtot[group] = 0;
+    if (threadIdx.x == 0) {
+      b.gtot[0][group] = 0;
+      b.gtot[1][group] = 0;
+    }
     // No fill of the successor tables: every read is confined to a state's
     // finite-successor range (irange), so layer 1 reads only the base entry
     // (g2 = 0, i = L) written below, and every later entry is written by the
@@ -285,6 +295,20 @@ __global__ void dp_prep(Batch b) {
       }
     for (int x = threadIdx.x; x < kParts * cw; x += blockDim.x)
       b.spart[(size_t)(x / cw) * b.n_groups * cw + (size_t)group * cw + x % cw] = 0u;
+  }
+  if (group == 0) {  // per (state, option j < 32): the option and its successor state
+    const int n = (b.G + 1) * 32;
+    const int x0 = n * part / kPrepY, x1 = n * (part + 1) / kPrepY;
+    for (int x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
+      const int g = x >> 5, j = x & 31;
+      const int r = b.g_mesh[g], o0 = b.opt_off[r], no = b.opt_off[r + 1] - o0;
+      int2 v = make_int2(-1, -1);
+      if (j < no) {
+        const int devs = b.opt_devs[o0 + j];
+        v = make_int2(o0 + j, devs <= b.g_avail[g] ? g - devs : -1);
+      }
+      b.gopt[x] = v;
+    }
   }
   __syncthreads();
   // suffix-min ranks are non-decreasing along a row: first entry no candidate
@@ -358,12 +382,12 @@ __global__ void dp_prep(Batch b) {
 // Per layer and group: the window [klo, khi] of every state g (cells outside
 // are provably infinite: no option can reach a finite successor from them),
 // the compact enumeration of the cells inside, and the reset of the irange
-// buffer layer s+1 writes (last read by layer s-1).  One thread per state,
-// kWinBlock states per block and blockIdx.y = group, so the per-state
-// dependent-load chains of a layer run on many SMs at once; each warp
-// reserves its states' cells in the group's list with one atomic (the order
-// of states in the list does not matter: cells are independent), and the
-// last block turns the group totals into goff.
+// buffer layer s+1 writes (last read by layer s-1).  One warp per state
+// (lane = option), kWinWarps states per block and blockIdx.y = group, so the
+// per-state dependent-load chains of a layer run on many SMs at once; each
+// warp reserves its state's cells in the group's list with one atomic (the
+// order of states in the list does not matter: cells are independent).
+// dp_relax_compact prefix-sums the group totals itself.
 constexpr int kWinWarps = 4;  // states per dp_window block (one warp each)
 __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
   pdl_wait();
@@ -376,25 +400,27 @@ __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
   // meshes): every option's loads are independent, the hull is a warp min/max
   int klo = 0x7fff, khi = 0;
   if (g <= G && g >= s) {
+    // option / successor state of lane j come precomputed (gopt), so the
+    // chain is gopt -> irange / spanlen -> the warp's hull
+    const int2 go = __ldg(b.gopt + (size_t)g * 32 + lane);
     const int4 gm = b.gmeta[g];
     int2 *wo = b.wopt + ((size_t)group * (G + 1) + g) * 32;
-    for (int j = lane; j < gm.y; j += 32) {
-      const int o = gm.x + j;
-      const int devs = __ldg(b.opt_devs + o), g2 = g - devs;
-      if (devs > gm.z || g2 < s - 1) {
-        if (j < 32) wo[j] = make_int2(1, 0);
-        continue;
+    auto option = [&](const int o, const int g2, const bool store) {
+      if (g2 < s - 1) {  // (also devs > available: g2 = -1)
+        if (store) wo[lane] = make_int2(1, 0);
+        return;
       }
       const int2 fr = b.irange[(s - 1) % 3][(size_t)group * (G + 1) + g2];
-      if (j < 32) wo[j] = make_int2(fr.x <= min(imax, fr.y) ? fr.x | (min(imax, fr.y) << 16) : 1,
-                                    g2 * (L + 1));
+      if (store)
+        wo[lane] = make_int2(fr.x <= min(imax, fr.y) ? fr.x | (min(imax, fr.y) << 16) : 1,
+                             g2 * (L + 1));
       const int mn = 0xffff - (int)__ldg(b.spanlen + ((size_t)group * 2 + 0) * b.n_opts + o);
       const int mx = (int)__ldg(b.spanlen + ((size_t)group * 2 + 1) * b.n_opts + o);
       // option o reaches a finite successor from cell k only through spans
       // (k, i) with i in [fr.x, min(fr.y, L-s+1)] and admissible length
       // i-k+1 in [minlen_o, maxlen_o]
       const int hi = min(imax, fr.y);
-      if (fr.x > hi || mx == 0) continue;
+      if (fr.x > hi || mx == 0) return;
       klo = min(klo, max(1, fr.x - mx + 1));
 #if HAPT_WIN_MINLEN
       khi = max(khi, hi - mn + 1);
@@ -402,6 +428,12 @@ __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
       (void)mn;
       khi = max(khi, hi);
 #endif
+    };
+    if (go.x >= 0) option(go.x, go.y, true);
+    for (int j = lane + 32; j < gm.y; j += 32) {  // meshes with more than 32 shapes
+      const int o = gm.x + j;
+      const int devs = __ldg(b.opt_devs + o);
+      option(o, devs <= gm.z ? g - devs : -1, false);
     }
   }
   klo = __reduce_min_sync(0xffffffffu, klo);
@@ -409,7 +441,7 @@ __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
   const int n = khi >= klo ? khi - klo + 1 : 0;
   if (g <= G) {
     int base = 0;
-    if (lane == 0 && n > 0) base = atomicAdd(b.gtot + group, n);
+    if (lane == 0 && n > 0) base = atomicAdd(b.gtot[s & 1] + group, n);
     base = __shfl_sync(0xffffffffu, base, 0);
     uint32_t *cl = b.clist + (size_t)group * b.ccap + base;
     for (int t = lane; t < n; t += 32) cl[t] = ((unsigned)g << 16) | (unsigned)(klo + t);
@@ -417,38 +449,8 @@ __global__ void __launch_bounds__(kWinWarps * 32) dp_window(Batch b, int s) {
       b.irange[(s + 1) % 3][(size_t)group * (G + 1) + g] = make_int2(0x7fffffff, -1);
     }
   }
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(b.ticket, 1u) == gridDim.x * gridDim.y - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  // last block (every reservation is in): exclusive prefix of the group
-  // totals, which are then zeroed for the next windowed layer
-  __threadfence();
-  int32_t *tot = b.gtot;
-  int run = 0;
-  for (int j0 = 0; j0 < b.n_groups; j0 += 32) {
-    const int j = j0 + lane;
-    const int v = (threadIdx.x < 32 && j < b.n_groups) ? __ldcg(tot + j) : 0;
-    int in2 = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, in2, off);
-      if (lane >= off) in2 += y;
-    }
-    if (threadIdx.x < 32 && j < b.n_groups) {
-      b.goff[j] = run + in2 - v;
-      tot[j] = 0;
-    }
-    run += __shfl_sync(0xffffffffu, in2, 31);
-  }
-  if (threadIdx.x == 0) {
-    b.goff[b.n_groups] = run;
-    *b.ticket = 0u;
-  }
+  // the next windowed layer's totals (last read by dp_relax(s-1), which completed)
+  if (blockIdx.x == 0 && threadIdx.x == 0) b.gtot[(s + 1) & 1][group] = 0;
 }
 
 template <int CPL>
@@ -933,17 +935,39 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   }
 }
 
-// Warp-collective: the group owning compact cell idx = largest j < ng with
-// goff[j] <= idx (goff non-decreasing, goff[0] = 0), 32 entries per step.
-__device__ __forceinline__ int find_group(const int32_t *__restrict__ goff, int ng, int idx,
-                                          int lane) {
-  for (int base = 0;; base += 32) {
-    const int j = base + 1 + lane;
-    const bool le = j < ng && __ldg(goff + j) <= idx;
-    const unsigned m = __ballot_sync(0xffffffffu, le);
-    if (m != 0xffffffffu) return base + __popc(m);
+// Warp-collective cursor over the compact cell index space of a layer: the
+// groups' window cells (gtot, dp_window) concatenated in group order.  A
+// warp's cells come in increasing index order, so the cursor only moves
+// forward, 32 groups at a time: lane j holds the inclusive prefix of group
+// base + j within the chunk (run = cells of the groups before the chunk).
+struct GroupCursor {
+  int base, run, incl, tot;
+  __device__ __forceinline__ void load(const int32_t *gtot, int ng, int lane) {
+    const int j = base + lane;
+    const int v = j < ng ? __ldg(gtot + j) : 0;
+    incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    tot = __shfl_sync(0xffffffffu, incl, 31);
   }
-}
+  // group owning cell idx (< the layer's total) and the index of the
+  // group's first cell
+  __device__ __forceinline__ int find(const int32_t *gtot, int ng, int idx, int lane,
+                                      int &first) {
+    while (idx >= run + tot) {
+      run += tot;
+      base += 32;
+      load(gtot, ng, lane);
+    }
+    const int j = __popc(__ballot_sync(0xffffffffu, run + incl <= idx));
+    const int ex = __shfl_sync(0xffffffffu, incl, (j + 31) & 31);
+    first = run + (j == 0 ? 0 : ex);
+    return base + j;
+  }
+};
 
 // Windowed layers: only the cells inside dp_window's windows, enumerated
 // compactly, one warp per cell over a grid capped at 256 warps per SM that
@@ -961,7 +985,16 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   __shared__ int4 stage_e[kWarps][32];
   __shared__ uint16_t stage_k[kWarps][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int total = b.goff[b.n_groups];
+  const int32_t *gtot = b.gtot[s & 1];
+  const int ng = b.n_groups;
+  GroupCursor gc{0, 0, 0, 0};
+  gc.load(gtot, ng, lane);
+  // the layer's total: the sum over every chunk of 32 groups
+  int total = gc.tot;
+  for (int j0 = 32; j0 < ng; j0 += 32) {
+    const int v = j0 + lane < ng ? __ldg(gtot + j0 + lane) : 0;
+    total += __reduce_add_sync(0xffffffffu, v);
+  }
   uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
   // this warp's finite-cell counts of its current group (shared memory, not
   // registers: the cell body is at the 64-register limit)
@@ -985,12 +1018,13 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     for (int c = 0; c < CPL; ++c) cnt[c] = 0u;
   };
   for (int idx = blockIdx.x * kWarps + warp; idx < total; idx += gridDim.x * kWarps) {
-    const int group = find_group(b.goff, b.n_groups, idx, lane);
+    int first;
+    const int group = gc.find(gtot, ng, idx, lane, first);
     if (group != cur) {
       if (cur >= 0) flush(cur);
       cur = group;
     }
-    const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - __ldg(b.goff + group)));
+    const unsigned gk = __ldg(b.clist + (size_t)group * b.ccap + (idx - first));
     const int g = (int)(gk >> 16), k = (int)(gk & 0xffffu);
     const int4 gm = b.gmeta[g];
     // this layer's split ranges of the state's first 32 options (dp_window)
@@ -1225,9 +1259,9 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.wopt = (int2 *)(wb + w.wopt);
   b.clist = (uint32_t *)(wb + w.clist);
   b.ccap = (size_t)t->L * t->G;
-  b.gtot = (int32_t *)(wb + w.gtot);
-  b.goff = (int32_t *)(wb + w.goff);
-  b.ticket = (unsigned *)(wb + w.ticket);
+  b.gtot[0] = (int32_t *)(wb + w.gtot[0]);
+  b.gtot[1] = (int32_t *)(wb + w.gtot[1]);
+  b.gopt = (int2 *)(wb + w.gopt);
   b.spart = (uint32_t *)(wb + w.spart);
   b.gmeta = (int4 *)(wb + w.gmeta);
   b.n_opts = t->n_opts;

@@ -28,6 +28,8 @@
 //    g2 < s-1) are never visited.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "hapt_common.cuh"
 
 namespace hapt {
@@ -44,6 +46,17 @@ __device__ unsigned long long g_work[8];  // executed / admissible / improving l
 #define HAPT_KWARPS 4
 #endif
 constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
+// dp_relax_compact: one-warp blocks (32 resident per SM at 64 registers), so
+// a finished warp's slot is refilled at once instead of idling until the
+// slowest warp of its block is done (round 2: C 2.19 -> 2.04 ms, D2 74.5 ->
+// 69.0 ms with the grid rule of run_sweep)
+#ifndef HAPT_KWARPS_C
+#define HAPT_KWARPS_C 1
+#endif
+#ifndef HAPT_RELAX_MINB_C
+#define HAPT_RELAX_MINB_C (32 / HAPT_KWARPS_C)
+#endif
+constexpr int kWarpsC = HAPT_KWARPS_C;  // warps per dp_relax_compact block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
 #ifndef HAPT_WIN_MINLEN
 #define HAPT_WIN_MINLEN 1  // window hull also bounded by each option's shortest span
@@ -158,7 +171,8 @@ struct Batch {
 };
 
 struct WsLayout {
-  size_t tmax_pad, tcnt, rowmeta, kc, ir[3], spanlen, wopt, clist, gtot[2], gopt, gmeta, spart, H0,
+  size_t tmax_pad, tcnt, rowmeta, kc, ir[3], spanlen, wopt, clist, gtot[2], gopt, gmeta, spart,
+      H0,
       H1, K0, K1, Hm0, Hm1, total;
 };
 
@@ -957,6 +971,11 @@ struct GroupCursor {
   // group's first cell
   __device__ __forceinline__ int find(const int32_t *gtot, int ng, int idx, int lane,
                                       int &first) {
+    if (idx < run) {  // (a claim that wrapped around to an earlier segment)
+      base = 0;
+      run = 0;
+      load(gtot, ng, lane);
+    }
     while (idx >= run + tot) {
       run += tot;
       base += 32;
@@ -977,13 +996,13 @@ struct GroupCursor {
 // group and go to one of kParts counter copies (dp_states_reduce sums them)
 // when it changes, so no warp waits at a block barrier for a slower one.
 template <int CPL>
-__global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
+__global__ void __launch_bounds__(kWarpsC * 32, HAPT_RELAX_MINB_C)
     dp_relax_compact(Batch b, int s) {
   pdl_wait();
   pdl_trigger();
   constexpr int CW = 32 * CPL;
-  __shared__ int4 stage_e[kWarps][32];
-  __shared__ uint16_t stage_k[kWarps][32];
+  __shared__ int4 stage_e[kWarpsC][32];
+  __shared__ uint16_t stage_k[kWarpsC][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t *gtot = b.gtot[s & 1];
   const int ng = b.n_groups;
@@ -998,7 +1017,7 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
   uint32_t *part = b.spart + (size_t)(blockIdx.x & (kParts - 1)) * b.n_groups * CW;
   // this warp's finite-cell counts of its current group (shared memory, not
   // registers: the cell body is at the 64-register limit)
-  __shared__ unsigned s_cnt[kWarps][CW];
+  __shared__ unsigned s_cnt[kWarpsC][CW];
   unsigned *cnt = &s_cnt[warp][lane * CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) cnt[c] = 0u;
@@ -1017,7 +1036,7 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
 #pragma unroll
     for (int c = 0; c < CPL; ++c) cnt[c] = 0u;
   };
-  for (int idx = blockIdx.x * kWarps + warp; idx < total; idx += gridDim.x * kWarps) {
+  auto cell = [&](const int idx) {
     int first;
     const int group = gc.find(gtot, ng, idx, lane, first);
     if (group != cur) {
@@ -1039,7 +1058,8 @@ __global__ void __launch_bounds__(kWarps * 32, HAPT_RELAX_MINB)
     relax_cell<CPL>(b, s, group, k, g, lane, stage_e[warp], stage_k[warp], fin, gm.x, gm.y, ol0);
 #pragma unroll
     for (int c = 0; c < CPL; ++c) cnt[c] += fin[c] ? 1u : 0u;
-  }
+  };
+  for (int idx = blockIdx.x * kWarpsC + warp; idx < total; idx += gridDim.x * kWarpsC) cell(idx);
   if (cur >= 0) flush(cur);
 }
 
@@ -1300,7 +1320,7 @@ int run_sweep(const Batch &b, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  unsigned gcap = (256u / kWarps) * (unsigned)sms;
+  unsigned gcap = 0;  // per layer below, unless HAPT_RELAX_GRID fixes it
   if (const char *e = getenv("HAPT_RELAX_GRID")) {
     const long v = atol(e);
     if (v >= 1 && v <= (1l << 20)) gcap = (unsigned)v;
@@ -1329,8 +1349,22 @@ int run_sweep(const Batch &b, cudaStream_t st) {
       // its upper bound, capped at 256 warps per SM that loop over the cells
       // (measured: launching the bound's mostly empty blocks cost ~4 % of a
       // D1 pool sweep; 128 warps per SM: +2.5 %, 512: +2.6 % at kWarps 8)
-      const unsigned cgrid = min(gcap, grid_for((size_t)cells * b.n_groups, kWarps));
-      const dim3 blk(kWarps * 32);
+      // The list's length is only known on the device: the grid is capped at
+      // a number of warps per SM that grows with the batch (L x G x groups /
+      // 2,300, between 64 and 192 per SM), and the warps stride over the
+      // list.  Surplus warps exit at once but still cost their dispatch; too
+      // few leave the tail unbalanced.  Measured with one-warp blocks
+      // (tools/gpu/grid_sweep.sh): D1 pool (294 K) 128 / SM 5.03 ms vs 256 / SM
+      // 5.20; D2 (1.1 M per half) 192 / SM 68.3 ms; D1 8-GPU share (73 K)
+      // 64 / SM 1.30 ms vs 128 / SM 1.47 ms.
+      unsigned cap = gcap;
+      if (cap == 0) {
+        const long wps =
+            (std::min(192l, std::max(64l, (long)b.L * b.G * b.n_groups / 2300)) + 16) / 32 * 32;
+        cap = (unsigned)(wps / kWarpsC) * (unsigned)sms;
+      }
+      const unsigned cgrid = min(cap, grid_for((size_t)cells * b.n_groups, kWarpsC));
+      const dim3 blk(kWarpsC * 32);
       ProfScope ps(kProfRelax, st);
       if (b.cpl == 1)
         HAPT_CUDA(launch_pdl(dp_relax_compact<1>, cgrid, blk, st, pdl, b, s));

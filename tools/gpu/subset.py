@@ -31,6 +31,21 @@ def main(name="D1", worlds="1,2,4,8", reps=10):
     for W in [int(x) for x in worlds.split(",")]:
         ps = PoolSharding.__new__(PoolSharding)
         ps.world = W
+        if os.environ.get("SUBSET_ALL_RANKS") and W > 1:
+            per = []
+            for r in range(W):
+                t = torch.from_numpy(pool[ps._positions(len(pool), r)]).cuda()
+                for _ in range(3):
+                    sw.sweep_device(t)
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                for _ in range(reps):
+                    sw.sweep_device(t)
+                e.record()
+                e.synchronize()
+                per.append(s.elapsed_time(e) / reps)
+            print(f"{name} W={W}: per-rank ms " + " ".join(f"{x:.3f}" for x in per), flush=True)
         pos = ps._positions(len(pool), 0)
         tm = torch.from_numpy(pool[pos]).cuda()
         for _ in range(3):

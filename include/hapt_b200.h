@@ -204,6 +204,15 @@ size_t hapt_dp_workspace_bytes(const hapt_tables *t, int32_t n_cand);
 int hapt_dp_sweep_batch(const hapt_tables *t, const double *tmax, int32_t n_cand,
                         double *ftop, int64_t *states, const hapt_dp_full *full,
                         void *work, size_t work_bytes, void *stream);
+/* hapt_dp_sweep_batch with the candidates per lane of the DP warps chosen
+ * by the caller: cpl = 1, 2 or 4 (0 = the library's choice from the batch and
+ * table sizes).  Results are identical for every choice; only speed differs.
+ * A batch whose t_max values are spread over the pool (the search's
+ * binary-search probes) runs fastest at 1: lanes with distant t_max share
+ * one warp's bounds.  work_bytes = hapt_dp_workspace_bytes covers every cpl. */
+int hapt_dp_sweep_batch_cpl(const hapt_tables *t, const double *tmax, int32_t n_cand,
+                            double *ftop, int64_t *states, const hapt_dp_full *full,
+                            void *work, size_t work_bytes, int32_t cpl, void *stream);
 
 /* Per candidate: best_s = first s minimising F[s,1,G] + (B-1)*t_max over
  * finite entries, tstar = that total (+inf if none) (planner.py:287-298).

@@ -127,6 +127,11 @@ _SIGNATURES = {
         c_i32,
         [ctypes.POINTER(Tables), c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(DpFull), c_vp, c_sz, c_vp],
     ),
+    "hapt_dp_sweep_batch_cpl": (
+        c_i32,
+        [ctypes.POINTER(Tables), c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(DpFull), c_vp, c_sz,
+         c_i32, c_vp],
+    ),
     "hapt_dp_select": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "hapt_dp_sweep_workspace_bytes": (c_sz, [ctypes.POINTER(Tables)]),
     "hapt_dp_sweep": (

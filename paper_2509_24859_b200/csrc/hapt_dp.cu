@@ -232,9 +232,9 @@ struct Split {
   size_t ws[2];  // aligned workspace bytes of each part
 };
 
-Split split_plan(const hapt_tables *t, int n_cand, bool full) {
+Split split_plan(const hapt_tables *t, int n_cand, bool full, int cpl = 0) {
   Split sp{};
-  sp.cpl = cpl_for(t, n_cand);
+  sp.cpl = cpl ? cpl : cpl_for(t, n_cand);
   const int cw = 32 * sp.cpl, ng = (n_cand + cw - 1) / cw;
   static const bool on = [] {
     const char *e = getenv("HAPT_SPLIT");
@@ -1415,10 +1415,15 @@ using namespace hapt;
 
 extern "C" size_t hapt_dp_workspace_bytes(const hapt_tables *t, int32_t n_cand) {
   if (!t || n_cand < 1) return 0;
-  const Split sp = split_plan(t, n_cand, false);
-  size_t total = 0;
-  for (int j = 0; j < sp.parts; ++j) total += sp.ws[j];
-  return max(total, align_up(ws_layout(t, n_cand).total));  // (full outputs: one part)
+  // enough for any candidates-per-lane choice (hapt_dp_sweep_batch_cpl)
+  size_t best = 0;
+  for (const int cpl : {1, 2, 4}) {
+    const Split sp = split_plan(t, n_cand, false, cpl);
+    size_t total = 0;
+    for (int j = 0; j < sp.parts; ++j) total += sp.ws[j];
+    best = max(best, max(total, align_up(ws_layout(t, n_cand, cpl).total)));  // (full: one part)
+  }
+  return best;
 }
 
 namespace {
@@ -1447,7 +1452,14 @@ int side_streams(cudaStream_t (&out)[2]) {
 extern "C" int hapt_dp_sweep_batch(const hapt_tables *t, const double *tmax, int32_t n_cand,
                                    double *ftop, int64_t *states, const hapt_dp_full *full,
                                    void *work, size_t work_bytes, void *stream) {
-  if (!t || !tmax || n_cand < 1 || !ftop || !states || !work) {
+  return hapt_dp_sweep_batch_cpl(t, tmax, n_cand, ftop, states, full, work, work_bytes, 0, stream);
+}
+
+extern "C" int hapt_dp_sweep_batch_cpl(const hapt_tables *t, const double *tmax, int32_t n_cand,
+                                       double *ftop, int64_t *states, const hapt_dp_full *full,
+                                       void *work, size_t work_bytes, int32_t cpl, void *stream) {
+  if (!t || !tmax || n_cand < 1 || !ftop || !states || !work ||
+      !(cpl == 0 || cpl == 1 || cpl == 2 || cpl == 4)) {
     set_error("hapt_dp_sweep_batch: invalid arguments");
     return HAPT_EINVAL;
   }
@@ -1456,7 +1468,8 @@ extern "C" int hapt_dp_sweep_batch(const hapt_tables *t, const double *tmax, int
     set_error("hapt_dp_sweep_batch: F/N need bp_i and bp_o, which go together");
     return HAPT_EINVAL;
   }
-  const Split sp = split_plan(t, n_cand, full != nullptr);
+  if (cpl == 0 || getenv("HAPT_CPL")) cpl = cpl_for(t, n_cand);  // (HAPT_CPL: experiments)
+  const Split sp = split_plan(t, n_cand, full != nullptr, cpl);
   size_t need = 0;
   for (int j = 0; j < sp.parts; ++j) need += sp.ws[j];
   if (work_bytes < need) {

@@ -268,9 +268,10 @@ class Sweeper:
         t = self.tables
         return 4 * n * (t.s_max + 1) * (t.L + 2) * (t.G + 1)
 
-    def sweep_device(self, tmax: torch.Tensor, full: DpFull | None = None):
+    def sweep_device(self, tmax: torch.Tensor, full: DpFull | None = None, cpl: int = 0):
         """tmax: float64 CUDA tensor [n].  Returns (ftop [n, s_max+1], states [n])
-        as device tensors; no host synchronisation."""
+        as device tensors; no host synchronisation.  cpl: candidates per lane
+        of the DP warps (0 = the library's choice; results never depend on it)."""
         t = self.tables
         n = int(tmax.numel())
         s1 = t.s_max + 1
@@ -284,7 +285,7 @@ class Sweeper:
             need = self.lib.hapt_dp_workspace_bytes(ctypes.byref(t.t), m)
             ws = self._workspace(need)
             check(
-                self.lib.hapt_dp_sweep_batch(
+                self.lib.hapt_dp_sweep_batch_cpl(
                     ctypes.byref(t.t),
                     tmax[c0:c1].data_ptr(),
                     m,
@@ -293,6 +294,7 @@ class Sweeper:
                     ctypes.byref(full) if full is not None else None,
                     ws.data_ptr(),
                     ws.numel(),
+                    int(cpl),
                     stream_ptr(),
                 )
             )
@@ -313,7 +315,7 @@ class Sweeper:
         return tstar, best_s, winner
 
     def evaluate(self, tmax_values, num_microbatches: int, keep_bp: bool = False,
-                 keep_ftop: bool = False) -> SweepResult:
+                 keep_ftop: bool = False, cpl: int = 0) -> SweepResult:
         """Sweep + select a batch; one host transfer for all per-candidate
         results.  keep_bp also records packed backpointers for every
         candidate (when they fit BP_BUDGET) so a winner can be walked without
@@ -328,7 +330,7 @@ class Sweeper:
             bp = torch.empty((n, t.s_max + 1, t.L + 2, t.G + 1), dtype=_I32, device=self.device)
             ntop = torch.zeros((n, t.s_max + 1), dtype=_I32, device=self.device)
             full = DpFull(None, None, None, None, bp.data_ptr(), ntop.data_ptr())
-        ftop, states = self.sweep_device(tmax, full=full)
+        ftop, states = self.sweep_device(tmax, full=full, cpl=cpl)
         tstar, best_s, winner = self.select_device(ftop, tmax, num_microbatches)
         parts = [tstar.view(torch.int64), best_s.to(torch.int64), states,
                  winner.to(torch.int64)]

@@ -26,7 +26,7 @@ class OracleSweeper:
     def bp_bytes(self, n):
         return 1
 
-    def evaluate(self, tmax_values, B, keep_bp=False, keep_ftop=False):
+    def evaluate(self, tmax_values, B, keep_bp=False, keep_ftop=False, cpl=0):  # (no lanes on CPU)
         import oracle as O
         from paper_2509_24859_b200.engine import SweepResult
 

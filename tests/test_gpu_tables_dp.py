@@ -124,6 +124,28 @@ def test_batch_chunking_is_invisible():
     assert np.array_equal(a.tstar, b.tstar) and np.array_equal(a.states, b.states)
 
 
+def test_caller_chosen_cpl_equals_reference():
+    """hapt_dp_sweep_batch_cpl: every candidates-per-lane choice, on the full
+    pool and on a spread batch like the search's probe trees, gives the
+    reference's per-candidate results."""
+    import torch
+
+    from paper_2509_24859_b200.planner import DpTables
+
+    for name in ("B", "C", "D1"):
+        inst, arr = load_json(name), expected_arrays(name)
+        store, costs, cluster, B, eps = build(inst)
+        tables = DpTables(store, costs)
+        pool = np.asarray(store.feasible_t_values())
+        for idx in (np.arange(len(pool)), np.arange(0, len(pool), 37)):
+            for cpl in (0, 1, 2, 4):
+                r = tables.sweeper.evaluate(pool[idx], B, cpl=cpl)
+                assert np.array_equal(r.tstar, arr["tstar"][idx]), (name, cpl)
+                assert np.array_equal(r.best_s, arr["best_s"][idx]), (name, cpl)
+                assert np.array_equal(r.states, arr["states"][idx]), (name, cpl)
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("env", [{"HAPT_CPL": "1"}, {"HAPT_CPL": "2"}, {"HAPT_CPL": "4"},
                                  {"HAPT_PROBE": "0"}])
 def test_every_kernel_variant_equals_reference(env):

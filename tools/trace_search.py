@@ -20,12 +20,12 @@ def main(names):
     log = []
     orig = engine.Sweeper.evaluate
 
-    def traced(self, tmax_values, B, keep_bp=False, keep_ftop=False):
+    def traced(self, tmax_values, B, keep_bp=False, keep_ftop=False, cpl=0):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = orig(self, tmax_values, B, keep_bp=keep_bp, keep_ftop=keep_ftop)
+        r = orig(self, tmax_values, B, keep_bp=keep_bp, keep_ftop=keep_ftop, cpl=cpl)
         torch.cuda.synchronize()
-        log.append((len(tmax_values), keep_bp, (time.perf_counter() - t0) * 1e3))
+        log.append((len(tmax_values), keep_bp, (time.perf_counter() - t0) * 1e3, cpl))
         return r
 
     engine.Sweeper.evaluate = traced
@@ -41,7 +41,7 @@ def main(names):
             torch.cuda.synchronize()
             tot = (time.perf_counter() - t) * 1e3
         print(f"{name}: search {tot:.2f} ms; batches " +
-              ", ".join(f"{n}{'+bp' if bp else ''}: {ms:.2f} ms" for n, bp, ms in log), flush=True)
+              ", ".join(f"{n}{'+bp' if bp else ''}(cpl {c}): {ms:.2f} ms" for n, bp, ms, c in log), flush=True)
 
 
 if __name__ == "__main__":

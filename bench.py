@@ -284,28 +284,64 @@ def workload_config(args) -> dict:
 
 
 class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled from NVML every
+    5 ms while it is entered (nvidia-smi as a fallback: one spawn takes
+    ~0.1 s, too coarse for a ~0.1 s timed region)."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.005):
         self.index = index
-        self.rows = []
+        self.period = period
+        self.rows = []  # (sm_mhz, max_mhz, [reason names])
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _sample_smi(self):
+        out = subprocess.run(
+            ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+             "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5,
+        ).stdout.strip()
+        if not out:
+            return None
+        r = [x.strip() for x in out.split(",")]
+        num = lambda x: float(x) if x.replace(".", "").isdigit() else None  # noqa: E731
+        return (num(r[0]), num(r[1]),
+                [self.NAMES[i] for i in range(4) if len(r) > 3 + i and r[3 + i].lower().startswith("active")])
+
     def _run(self):
+        nv = h = None
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001
+            nv = None
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5,
-                ).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if nv is not None:
+                    sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    ev = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((sm, mx, [self.NAMES[i] for i, b in enumerate(bits) if ev & b]))
+                else:
+                    row = self._sample_smi()
+                    if row:
+                        self.rows.append(row)
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(self.period)
+        if nv is not None:
+            try:
+                nv.nvmlShutdown()
+            except Exception:  # noqa: BLE001
+                pass
 
     def __enter__(self):
         self._t.start()
@@ -318,13 +354,11 @@ class ClockSampler:
     def summary(self) -> dict:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit()
-                else None, "reasons": reasons, "samples": len(self.rows)}
+        sm = sorted(r[0] for r in self.rows if r[0] is not None)
+        reasons = sorted({n for r in self.rows for n in r[2]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.rows[0][1],
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML, 5 ms period, warm-up through the timed steps"}
 
 
 def kernel_roofline(args, lib, torch, device, step, flush, tables, store, mine, ms_per_step,

@@ -126,6 +126,41 @@ class PoolSharding:
             return tstar, best_s, states, ftop
         return tstar, best_s, states
 
+    def gather_positions(self, local: torch.Tensor, n: int) -> torch.Tensor:
+        """All ranks' per-candidate rows, device to device: local [m, C] int64
+        holds this rank's candidates in shard_positions(n) order; returns
+        [n, C] in pool order on every rank (one all_gather of equally padded
+        blocks, then a scatter by the deal's positions)."""
+        key = (n, self.world)
+        cache = getattr(self, "_pos_cache", None)
+        if cache is None or cache[0] != key:
+            pos = [self._positions(n, r) for r in range(self.world)]
+            cache = (key, pos, {})
+            self._pos_cache = cache
+        pos, dev_idx = cache[1], cache[2]
+        dev = self.device
+        width = max(1, max(len(p) for p in pos))
+        C = local.shape[1]
+        pad = torch.zeros((width, C), dtype=local.dtype, device=dev)
+        pad[: local.shape[0]] = local.to(dev)
+        if self.backend == "nccl":
+            out = torch.empty((self.world * width, C), dtype=local.dtype, device=dev)
+            dist.all_gather_into_tensor(out, pad, group=self.group)
+            out = out.view(self.world, width, C)
+        else:
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            dist.all_gather(parts, pad, group=self.group)
+            out = torch.stack(parts)
+        self.collective_calls += 1
+        if dev not in dev_idx:
+            sel = np.concatenate([r * width + np.arange(len(p)) for r, p in enumerate(pos)])
+            dst = np.concatenate(pos)
+            dev_idx[dev] = (torch.from_numpy(sel).to(dev), torch.from_numpy(dst).to(dev))
+        sel, dst = dev_idx[dev]
+        full = torch.empty((n, C), dtype=local.dtype, device=dev)
+        full[dst] = out.reshape(-1, C)[sel]
+        return full
+
     def allreduce_argmin_device(self, tstar: torch.Tensor, winner: torch.Tensor,
                                 global_index: torch.Tensor):
         """Device-side allreduce-argmin of a sweep's local winner, no host

@@ -635,15 +635,38 @@ def sweep_pool(store: ProfileStore, costs: BoundaryCost, num_microbatches: int, 
                           best_s.to(torch.int64), states, winner.to(torch.int64)]).cpu().numpy()
         return (host[:n].view(np.float64).copy(), host[n:2 * n].view(np.float64).copy(),
                 host[2 * n:3 * n].copy(), host[3 * n:4 * n].copy(), int(host[4 * n]))
-    pool = candidate_tmax(store)
-    ev = CandidateEvaluator(tables, pool, num_microbatches, dist)
-    ev.ensure(range(len(pool)), keep_bp=False)  # no plan is built from a pool sweep
-    feas = np.where(ev.best_s >= 0)[0]
-    winner = -1
-    if len(feas):
-        order = np.lexsort((ev.pool[feas], ev.tstar[feas]))
-        winner = int(feas[order[0]])
-    return ev.pool, ev.tstar, ev.best_s, ev.states, winner
+    # Sharded: the pool stays on the device; each rank sweeps its blocks, the
+    # per-candidate results are all-gathered device to device and scattered
+    # back into pool order, the (T*, index) argmin is taken on the device,
+    # and everything comes back in one transfer -- the pool count is the only
+    # other host read.
+    import torch
+
+    n = store.dev.pool_len
+    if n == 0:
+        raise InfeasiblePlanError("no feasible candidates in the profile store")
+    sw = tables.sweeper
+    pool_dev = store.dev.pool()
+    mine = torch.from_numpy(dist.shard_positions(n)).to(pool_dev.device)
+    if mine.numel():
+        tmax = pool_dev[mine].contiguous()
+        ftop, states = sw.sweep_device(tmax)
+        tstar, best_s, _ = sw.select_device(ftop, tmax, num_microbatches)
+        local = torch.stack([tstar.view(torch.int64), best_s.to(torch.int64), states], dim=1)
+    else:
+        local = torch.zeros((0, 3), dtype=torch.int64, device=pool_dev.device)
+    full = dist.gather_positions(local, n)  # [n, 3] in pool order
+    t_bits, bs = full[:, 0], full[:, 1]
+    big = torch.iinfo(torch.int64).max
+    key = torch.where(bs >= 0, t_bits, torch.full_like(t_bits, big))
+    kmin = key.min()
+    ar = torch.arange(n, dtype=torch.int64, device=key.device)
+    win = torch.where(key == kmin, ar, torch.full_like(ar, big)).min()
+    win = torch.where(kmin == big, torch.full_like(win, -1), win)
+    host = torch.cat([pool_dev.view(torch.int64).to(full.device), full.t().reshape(-1),
+                      win.reshape(1)]).cpu().numpy()
+    return (host[:n].view(np.float64).copy(), host[n:2 * n].view(np.float64).copy(),
+            host[2 * n:3 * n].copy(), host[3 * n:4 * n].copy(), int(host[4 * n]))
 
 
 def _score(sweeper, ftop: np.ndarray, tmax: np.ndarray, B: int):

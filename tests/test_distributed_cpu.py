@@ -82,8 +82,12 @@ def _worker(rank, world, port, name, out_q, min_shard):
             torch.from_numpy(np.ascontiguousarray(res.tstar, dtype=np.float64)),
             torch.tensor([w], dtype=torch.int32), torch.tensor(mine, dtype=torch.int64))
         d_t = float(np.array([int(d_bits)], dtype=np.int64).view(np.float64)[0])
+        # sweep_pool(dist)'s device-to-device gather of the per-candidate rows
+        local = torch.from_numpy(np.stack([np.ascontiguousarray(res.tstar).view(np.int64),
+                                           res.best_s, res.states], axis=1))
+        full = sh.gather_positions(local, len(pool)).numpy()
         out_q.put((rank, lo, surv, best, float(ev.tstar[best]), g_t, g_i, sum(sw.calls),
-                   sh.collective_calls, d_t, int(d_idx)))
+                   sh.collective_calls, d_t, int(d_idx), full))
     finally:
         dist.destroy_process_group()
 
@@ -108,7 +112,7 @@ def test_two_rank_search_and_argmin(name, min_shard):
              for r in range(2)]
     for p in procs:
         p.start()
-    results = sorted(q.get(timeout=300) for _ in procs)
+    results = sorted((q.get(timeout=300) for _ in procs), key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -116,7 +120,10 @@ def test_two_rank_search_and_argmin(name, min_shard):
     arr = expected_arrays(name)
     pool = arr["pool"]
     ref_plan = exp["plan"]
-    for rank, lo, surv, best, tstar, g_t, g_i, n_eval, n_coll, d_t, d_i in results:
+    for rank, lo, surv, best, tstar, g_t, g_i, n_eval, n_coll, d_t, d_i, full in results:
+        assert np.array_equal(full[:, 0].view(np.float64), arr["tstar"])
+        assert np.array_equal(full[:, 1], arr["best_s"])
+        assert np.array_equal(full[:, 2], arr["states"])
         assert tstar == ref_plan["predicted_latency"]
         assert pool[best] == ref_plan["t_max"]
         assert lo == ref_plan["search_stats"]["pruned_below_ts"]

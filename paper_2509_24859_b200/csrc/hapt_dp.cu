@@ -130,7 +130,9 @@ struct Batch {
   const double *tmax;  // [n_cand]
   double *tmax_pad;    // [n_groups*cw]
   int32_t *tcnt;       // [n_groups*cw]  #pool values <= t_max
-  uint2 *rowmeta;      // [n_groups][rows] {span_off of the row, cut | kmin << 16}:
+  uint4 *rowmeta;      // [n_groups][rows] {span_off of the row, cut | kmin << 16,
+                       //  span_off - first split (INT_MIN if the row's splits are
+                       //  not consecutive), 0}:
                        // cut = entries of the row before its suffix-min pool rank
                        // reaches the group's largest bound, kmin = row_kmin (one
                        // 8-byte load per option in the cell prologue)
@@ -185,7 +187,7 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand, int cpl) {
   size_t cur = 0;
   w.tmax_pad = cur; cur += align_up(np * 8);
   w.tcnt = cur; cur += align_up(np * 4);
-  w.rowmeta = cur; cur += align_up(ng * rows * 8);
+  w.rowmeta = cur; cur += align_up(ng * rows * 16);
   w.kc = cur; cur += align_up(ng * 2 * t->n_meshes * (t->L + 1) * cw);
   for (int j = 0; j < 3; ++j) {
     w.ir[j] = cur;
@@ -340,8 +342,18 @@ __global__ void dp_prep(Batch b) {
       const int mid = (lo + hi) >> 1;
       if (b.span_srank[mid] < gm) lo = mid + 1; else hi = mid;
     }
+    // a row's feasible splits form one run i0, i0+1, ... (OOM bounds a span
+    // from above, the imbalance test from both sides), so entry p of the
+    // row ends at i0 + p and its successor needs no span load (staging);
+    // d0 = span_off - i0, INT_MIN where the run has gaps (overrides)
+    int d0 = (int)0x80000000;
+    if (end > beg) {
+      const int i0 = (int)b.spans[beg].i;
+      if ((int)b.spans[end - 1].i - i0 + 1 == end - beg) d0 = beg - i0;
+    }
     b.rowmeta[(size_t)group * b.rows + row] =
-        make_uint2((unsigned)beg, (unsigned)(lo - beg) | ((unsigned)b.row_kmin[row] << 16));
+        make_uint4((unsigned)beg, (unsigned)(lo - beg) | ((unsigned)b.row_kmin[row] << 16),
+                   (unsigned)d0, 0u);
     if (lo > beg) {
       const int o = row / (b.L + 2), k = row - o * (b.L + 2);
       atomicMax(b.spanlen + ((size_t)group * 2 + 0) * b.n_opts + o,
@@ -507,6 +519,9 @@ __device__ __forceinline__ void load_k(const char *p, int (&k)[CPL]) {
 // unroll with inert entries (w2 = ~0 never passes), so the loop has no
 // guards.  Every candidate keeps the first strict minimum, exactly the
 // reference's `cand < best` update.
+#ifndef HAPT_SPEC_CPL4
+#define HAPT_SPEC_CPL4 0
+#endif
 __device__ __forceinline__ void prefetch_l1(const void *p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -658,15 +673,16 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     const int nch = min(32, nopt - c0);
     const int o = o0 + c0 + lane;
     // lane j: admissible entries of option o's row (k) at this layer
-    int len = 0, beg = 0;
+    int len = 0, beg = 0, d0 = (int)0x80000000;
     bool needkk = false;
     const int lo_i = max(k, ol.fr & 0xffff), hi_i = (int)((unsigned)ol.fr >> 16);
     if (lane < nch && lo_i <= hi_i) {
       const int row = o * (L + 2) + k;
       // admissible splits also end at i <= L-s+1 (later successors are
       // provably infinite) and before the group's suffix-rank cut
-      const uint2 rm = __ldg(b.rowmeta + (size_t)group * b.rows + row);
+      const uint4 rm = __ldg(b.rowmeta + (size_t)group * b.rows + row);
       const int soff = (int)rm.x, cut = (int)(rm.y & 0xffffu), kmin = (int)(rm.y >> 16);
+      d0 = (int)rm.z;
       const uint16_t *pos = b.row_pos + (size_t)row * (L + 2);
       const int a = __ldg(pos + lo_i - 1);
       const int z = min((int)__ldg(pos + hi_i), cut);
@@ -686,6 +702,9 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
     }
     const int T = __shfl_sync(0xffffffffu, incl, 31);
     const int start = incl - len;
+    // successor of flattened entry t of this row = hsp + t (consecutive
+    // splits), so its bound load need not wait for the span entry
+    const int hsp = d0 != (int)0x80000000 ? hbase + beg - start - d0 : (int)0x80000000;
 #ifdef HAPT_COUNT_WORK
     if (lane == 0 && c0 == 0) {
       atomicAdd(&g_work[4], 1ull);
@@ -726,14 +745,19 @@ __device__ __forceinline__ void relax_cell(const Batch &b, int s, int group, int
       const int ob = __shfl_sync(0xffffffffu, beg, jj);
       const int os = __shfl_sync(0xffffffffu, start, jj);
       const int oh = __shfl_sync(0xffffffffu, hbase, jj);
+      const int hs = __shfl_sync(0xffffffffu, hsp, jj);
       int4 se = make_int4(0, 0, -1, 0);  // inert padding entry
       uint16_t sk = 0;
       bool keep = false;
       double lb = kInf;  // tt + Hmin: no lane's value through this entry is lower
       if (t < T) {
+        double hmv = 0.0;
+        const bool spec = HAPT_SPEC_CPL4 || CPL < 4 ? hs != (int)0x80000000 : false;
+        if (spec) hmv = __ldg(Hm + hs + t);
         const int4 x = __ldg(reinterpret_cast<const int4 *>(b.spans + ob + (t - os)));
         const int succ = oh + (x.w & 0xffff);
-        lb = __dadd_rn(__hiloint2double(x.y, x.x), __ldg(Hm + succ));
+        if (!spec) hmv = __ldg(Hm + succ);
+        lb = __dadd_rn(__hiloint2double(x.y, x.x), hmv);
         keep = lb < bmax;
         // w2 = pool rank (INT32_MAX for a non-finite t: never below a count)
         se = make_int4(x.x, x.y, x.z, succ * (256 * CPL));
@@ -1289,7 +1313,7 @@ Batch make_batch(const hapt_tables *t, const double *tmax, int n_cand, double *f
   b.tmax = tmax;
   b.tmax_pad = (double *)(wb + w.tmax_pad);
   b.tcnt = (int32_t *)(wb + w.tcnt);
-  b.rowmeta = (uint2 *)(wb + w.rowmeta);
+  b.rowmeta = (uint4 *)(wb + w.rowmeta);
   b.kc = (uint8_t *)(wb + w.kc);
   b.cb_rows = 2 * t->n_meshes;
   for (int j = 0; j < 3; ++j) b.irange[j] = (int2 *)(wb + w.ir[j]);

@@ -78,6 +78,34 @@ def test_dp_sweep_dropin_matches_reference_kernel():
     assert n > 10
 
 
+def test_rows_with_split_gaps_equal_oracle():
+    """K1 rows hold consecutive splits (the staging computes a successor
+    from the entry's position); a CSR with gaps -- possible through the
+    drop-in operator's caller-built span index -- takes the load-based path
+    and still equals the reference algorithm."""
+    from paper_2509_24859_b200._core import dp_sweep
+
+    tb = dict(O.tables(load_json("B")))
+    off, items = np.asarray(tb["span_off"]), np.asarray(tb["span_items"])
+    keep = np.ones(len(items), dtype=bool)
+    for r in range(len(off) - 1):
+        if off[r + 1] - off[r] >= 3:
+            keep[off[r] + 1] = False  # drop each long row's second split
+    counts = np.diff(off)
+    new_counts = np.array([keep[off[r]:off[r + 1]].sum() for r in range(len(counts))])
+    tb["span_items"] = np.ascontiguousarray(items[keep], dtype=np.int32)
+    tb["span_off"] = np.ascontiguousarray(np.concatenate([[0], np.cumsum(new_counts)]),
+                                          dtype=np.int32)
+    assert keep.sum() < len(items)
+    for t in tb["pool"][::11]:
+        got = dp_sweep(t, tb["t_tab"], tb["mp_tab"], tb["ma_tab"], tb["opt_cap"], tb["opt_mesh"],
+                       tb["opt_devs"], tb["opt_off"], tb["cb_same"], tb["cb_next"], tb["g_mesh"],
+                       tb["g_avail"], tb["s_max"], tb["span_off"], tb["span_items"])
+        want = O.dp_sweep(tb, t)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w)
+
+
 @pytest.mark.parametrize("name", ["A", "B"])
 def test_dp_sweep_dropin_full_pool_equals_oracle(name):
     from paper_2509_24859_b200._core import dp_sweep

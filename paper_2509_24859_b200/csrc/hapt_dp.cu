@@ -1031,8 +1031,9 @@ struct GroupCursor {
 };
 
 // Windowed layers: only the cells inside dp_window's windows, enumerated
-// compactly, one warp per cell over a grid capped at 256 warps per SM that
-// strides over the list -- no warp is spent on a provably infinite cell, and
+// compactly, one warp per cell over a grid of one-warp blocks (capped per SM
+// by run_sweep) that strides over the list -- no warp is spent on a provably
+// infinite cell, and
 // the state's per-option split ranges come precomputed from dp_window.
 // Finite-cell counts stay in shared memory while a warp's cells stay in one
 // group and go to one of kParts counter copies (dp_states_reduce sums them)
@@ -1358,7 +1359,7 @@ int run_sweep(const Batch &b, cudaStream_t st) {
     ProfScope ps(kProfOther, st);  // block >= 128 = max group width
     HAPT_CUDA(launch_pdl(dp_prep, dim3(b.n_groups, kPrepY), 256, st, pdl, b));
   }
-  // grid cap of dp_relax_compact: 256 warps per SM, per device
+  // SM count of this device (dp_relax_compact's grid cap, per layer below)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1387,10 +1388,6 @@ int run_sweep(const Batch &b, cudaStream_t st) {
         ProfScope ps(kProfWindow, st);
         HAPT_CUDA(launch_pdl(dp_window, wgrid, kWinWarps * 32, st, pdl, b, s));
       }
-      // the compact list's length is only known on the device: the grid is
-      // its upper bound, capped at 256 warps per SM that loop over the cells
-      // (measured: launching the bound's mostly empty blocks cost ~4 % of a
-      // D1 pool sweep; 128 warps per SM: +2.5 %, 512: +2.6 % at kWarps 8)
       // The list's length is only known on the device: the grid is capped at
       // a number of warps per SM that grows with the batch (L x G x groups /
       // 2,300, between 64 and 192 per SM), and the warps stride over the

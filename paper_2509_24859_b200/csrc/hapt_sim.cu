@@ -24,6 +24,8 @@
 // (the reference tests corrupt one to provoke CycleError): a single-CTA
 // frontier Kahn sweep with atomicMax on the (non-negative) double bit
 // patterns.
+#include <stdlib.h>
+
 #include "hapt_common.cuh"
 
 namespace hapt {
@@ -455,6 +457,121 @@ __global__ void __launch_bounds__(SimCfg<S>::threads)
   status[p] = HAPT_OK;
 }
 
+// Makespan-only variant for 5-8 stages: one lane per stage, S consecutive
+// lanes per plan (32 / S plans per warp).  Every round each lane tries the next op of its
+// stage's program with the same readiness rules as k_sim_s (neighbours'
+// progress read by shuffles at the start of the round, transfers through
+// per-link FIFOs in shared memory, written in a round and read in a later
+// one), so a plan advances up to S ops per round instead of one thread
+// walking all S stages; the max-plus times are the same whatever the order.
+// A plan none of whose lanes can move in a round is deadlocked or exceeds
+// the FIFO depth and goes to the generic kernel, like k_sim_s's.
+#ifndef HAPT_SIM_LANES_MIN
+#define HAPT_SIM_LANES_MIN 7  // (S = 5, 6: k_sim_s measured faster -- 5.26 vs 5.10 ms per 10^6 config-E plans)
+#endif
+template <int S>
+struct LaneCfg {
+  static constexpr int per_warp = 32 / S;    // plans per warp
+  static constexpr int plans = 4 * per_warp;  // plans per 128-thread block
+};
+template <int S>
+__global__ void __launch_bounds__(128)
+    k_sim_l(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
+            const double *t_bwd, const double *comm, const int32_t *counts,
+            const int32_t *num_mb, double *makespan, int32_t *status) {
+  constexpr int PW = LaneCfg<S>::per_warp;
+  __shared__ double ring[LaneCfg<S>::plans][S > 1 ? S - 1 : 1][2][kRing];
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / S, s = lane - sub * S, slot = (threadIdx.x >> 5) * PW + sub;
+  const int t = blockIdx.x * LaneCfg<S>::plans + slot;
+  const unsigned gmask = ((1u << S) - 1u) << (sub * S);
+  const bool has = sub < PW && t < n;
+  const int p = has ? perm[t] : 0;
+  const bool act = has && s < S;
+  const int b0 = has ? stage_off[p] : 0, B = has ? num_mb[p] : 1;
+  int N = 1;
+  double tf = 0.0, tb = 0.0, cmf = 0.0, cmb = 0.0;
+  if (act) {
+    N = counts[b0 + s];
+    tf = t_fwd[b0 + s];
+    tb = t_bwd[b0 + s];
+    if (s + 1 < S) cmf = comm[b0 + s];
+    if (s > 0) cmb = comm[b0 + s - 1];
+  }
+  // build_program preconditions (scheduling.py:235-239, 61-66)
+  const bool bad = has && (B < 1 || (act && (N < 1 || N > B)) || (s == S - 1 && N != 1));
+  const bool plan_bad = (__ballot_sync(0xffffffffu, bad) & gmask) != 0;
+  if (plan_bad && s == 0) status[p] = HAPT_ESCHED;
+  bool done = !act || plan_bad, stuck = false;
+  int pos = 0, fd = 0, bd = 0;
+  double prev = 0.0, lcf = 0.0, lcb = 0.0, mk = 0.0;
+  double(*rg)[2][kRing] = ring[sub < PW ? slot : 0];
+  for (;;) {
+    const unsigned alive = __ballot_sync(0xffffffffu, !done);
+    if (alive == 0u) break;
+    const int fd_l = __shfl_up_sync(0xffffffffu, fd, 1), bd_l = __shfl_up_sync(0xffffffffu, bd, 1);
+    const int fd_r = __shfl_down_sync(0xffffffffu, fd, 1);
+    const int bd_r = __shfl_down_sync(0xffffffffu, bd, 1);
+    bool ready = false, isF = false;
+    int mb = 0;
+    if (!done) {
+      mb = decode_op(pos, N, B, isF);
+      if (isF)
+        ready = (s == 0 || fd_l >= mb) && (s == S - 1 || mb - fd_r <= kRing);
+      else
+        ready = (s == S - 1 || bd_r >= mb) && (s == 0 || mb - bd_l <= kRing);
+    }
+    if (ready) {
+      double dep = 0.0;
+      if (isF && s > 0) dep = rg[s - 1][0][mb & (kRing - 1)];
+      if (!isF && s < S - 1) dep = rg[s][1][mb & (kRing - 1)];
+      const double st = fmax(prev, dep);
+      const double en = __dadd_rn(st, isF ? tf : tb);
+      prev = en;
+      mk = fmax(mk, en);
+      if (isF) {
+        fd = mb;
+        if (s < S - 1) {  // forward transfer on link s (simulation.py:130-140)
+          const double ce = __dadd_rn(fmax(en, lcf), cmf);
+          lcf = ce;
+          mk = fmax(mk, ce);
+          rg[s][0][mb & (kRing - 1)] = ce;
+        }
+      } else {
+        bd = mb;
+        if (s > 0) {  // backward transfer on link s-1
+          const double ce = __dadd_rn(fmax(en, lcb), cmb);
+          lcb = ce;
+          mk = fmax(mk, ce);
+          rg[s - 1][1][mb & (kRing - 1)] = ce;
+        }
+      }
+      if (++pos == 2 * B) done = true;
+    }
+    // a plan with live lanes none of which could move will never move
+    const unsigned moved = __ballot_sync(0xffffffffu, ready);
+    if ((alive & gmask) && !(moved & gmask)) {
+      stuck = true;
+      done = true;
+    }
+    __syncwarp();  // this round's FIFO writes before the next round's reads
+  }
+  // the plan's makespan: max over its lanes, gathered on its first lane
+#pragma unroll
+  for (int j = 1; j < S; ++j) {
+    const double v = __shfl_down_sync(0xffffffffu, mk, j);
+    if (s + j < S) mk = fmax(mk, v);
+  }
+  if (has && s == 0 && !plan_bad) {
+    if (stuck) {
+      status[p] = kRetry;
+    } else {
+      makespan[p] = mk;
+      status[p] = HAPT_OK;
+    }
+  }
+}
+
 // Counting sort of plan indices by stage count (bucket S for 1..8, bucket 0
 // for S > 8): per-block histograms, one scan, per-block scatter.  Order inside
 // a bucket is irrelevant (plans are independent).
@@ -533,6 +650,18 @@ void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const do
   }
   const unsigned grid = grid_for(n, C::threads);
   const int m = out.mode();
+  static const bool lanes = [] {
+    const char *e = getenv("HAPT_SIM_LANES");
+    return !(e && e[0] == '0');
+  }();
+  if constexpr (S >= HAPT_SIM_LANES_MIN && S <= 8) {
+    if (m == kNoNodes && lanes) {
+      k_sim_l<S><<<grid_for(n, LaneCfg<S>::plans), 128, 0, st>>>(perm, n, stage_off, t_fwd, t_bwd, comm,
+                                                         counts, num_mb, makespan, status);
+      ::hapt::note_launch();
+      return;
+    }
+  }
   if (m == kTrace)
     k_sim_s<S, kTrace><<<grid, C::threads, C::smem, st>>>(
         perm, n, stage_off, t_fwd, t_bwd, comm, counts, num_mb, makespan, status, out);

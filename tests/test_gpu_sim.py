@@ -95,6 +95,41 @@ def test_simulate_batch_config_e_equals_oracle():
         assert mk[p] == want, p
 
 
+@pytest.mark.parametrize("B", [4, 17, 64])
+def test_simulate_batch_many_stages_equals_oracle(B):
+    """7- and 8-stage plans (one lane per stage, k_sim_l) and 5-6-stage ones
+    (k_sim_s), with non-increasing launch counts from B down to 1 --
+    including steps between neighbouring stages deeper than the transfer
+    FIFOs, which hand the plan to the generic kernel -- against the
+    oracle's explicit DAG."""
+    from paper_2509_24859_b200.simulation import simulate_batch
+
+    rng = np.random.default_rng(1000 + B)
+    P = 600
+    S = rng.choice(np.array([5, 6, 7, 8]), size=P).astype(np.int32)
+    f = rng.uniform(0.5, 2.0, size=(P, 8)) * 1e-2
+    b = f * rng.uniform(1.5, 2.5, size=(P, 8))
+    c = rng.uniform(0.0, 1e-2, size=(P, 8))
+    dense = np.zeros((P, 8), dtype=np.int32)
+    for p in range(P):
+        s_ = int(S[p])
+        n = np.sort(rng.integers(1, B + 1, size=s_))[::-1].copy()  # non-increasing
+        if p % 3 == 0:  # the reference's small steps (delta in 1..3)
+            n = 1 + np.concatenate([np.cumsum(rng.integers(1, 4, size=s_ - 1)[::-1])[::-1], [0]])
+            n = np.minimum(n, B)
+        n[-1] = 1
+        dense[p, :s_] = n
+        f[p, s_:] = b[p, s_:] = 0.0
+        c[p, s_ - 1:] = 0.0
+    mk, st = simulate_batch(f, b, c, dense, B, stage_counts=S)
+    mk, st = mk.cpu().numpy(), st.cpu().numpy()
+    assert (st == 0).all()
+    for p in range(P):
+        s_ = int(S[p])
+        want, _, _ = O.simulate(f[p, :s_], b[p, :s_], c[p, : s_ - 1], list(dense[p, :s_]), B)
+        assert mk[p] == want, (p, s_, list(dense[p, :s_]))
+
+
 def test_launch_counts_kinds_and_errors():
     from paper_2509_24859_b200.scheduling import (CommTooLargeError, ScheduleError,
                                                   adaptive_counts, launch_counts_batch)

@@ -474,11 +474,11 @@ struct LaneCfg {
   static constexpr int per_warp = 32 / S;    // plans per warp
   static constexpr int plans = 4 * per_warp;  // plans per 128-thread block
 };
-template <int S>
+template <int S, int M>  // M: kNoNodes / kRefNodes / kTrace, as k_sim_s
 __global__ void __launch_bounds__(128)
     k_sim_l(const int32_t *perm, int n, const int32_t *stage_off, const double *t_fwd,
             const double *t_bwd, const double *comm, const int32_t *counts,
-            const int32_t *num_mb, double *makespan, int32_t *status) {
+            const int32_t *num_mb, double *makespan, int32_t *status, NodeOut out) {
   constexpr int PW = LaneCfg<S>::per_warp;
   __shared__ double ring[LaneCfg<S>::plans][S > 1 ? S - 1 : 1][2][kRing];
   const int lane = threadIdx.x & 31;
@@ -506,6 +506,8 @@ __global__ void __launch_bounds__(128)
   int pos = 0, fd = 0, bd = 0;
   double prev = 0.0, lcf = 0.0, lcb = 0.0, mk = 0.0;
   double(*rg)[2][kRing] = ring[sub < PW ? slot : 0];
+  constexpr bool nodes = M != kNoNodes;
+  const int64_t nb = nodes && act ? out.off[p] : 0;
   for (;;) {
     const unsigned alive = __ballot_sync(0xffffffffu, !done);
     if (alive == 0u) break;
@@ -529,21 +531,26 @@ __global__ void __launch_bounds__(128)
       const double en = __dadd_rn(st, isF ? tf : tb);
       prev = en;
       mk = fmax(mk, en);
+      if (nodes) out.op<M>(nb, B, s, mb, isF, pos, st, en);
       if (isF) {
         fd = mb;
         if (s < S - 1) {  // forward transfer on link s (simulation.py:130-140)
-          const double ce = __dadd_rn(fmax(en, lcf), cmf);
+          const double cs = fmax(en, lcf);
+          const double ce = __dadd_rn(cs, cmf);
           lcf = ce;
           mk = fmax(mk, ce);
           rg[s][0][mb & (kRing - 1)] = ce;
+          if (nodes) out.xfer<M>(nb, S, B, s, 0, mb, cs, ce);
         }
       } else {
         bd = mb;
         if (s > 0) {  // backward transfer on link s-1
-          const double ce = __dadd_rn(fmax(en, lcb), cmb);
+          const double cs = fmax(en, lcb);
+          const double ce = __dadd_rn(cs, cmb);
           lcb = ce;
           mk = fmax(mk, ce);
           rg[s - 1][1][mb & (kRing - 1)] = ce;
+          if (nodes) out.xfer<M>(nb, S, B, s - 1, 1, mb, cs, ce);
         }
       }
       if (++pos == 2 * B) done = true;
@@ -566,6 +573,7 @@ __global__ void __launch_bounds__(128)
     if (stuck) {
       status[p] = kRetry;
     } else {
+      if (nodes) out.sink<M>(nb, S, B, mk);
       makespan[p] = mk;
       status[p] = HAPT_OK;
     }
@@ -655,9 +663,17 @@ void launch_sim_s(const int32_t *perm, int n, const int32_t *stage_off, const do
     return !(e && e[0] == '0');
   }();
   if constexpr (S >= HAPT_SIM_LANES_MIN && S <= 8) {
-    if (m == kNoNodes && lanes) {
-      k_sim_l<S><<<grid_for(n, LaneCfg<S>::plans), 128, 0, st>>>(perm, n, stage_off, t_fwd, t_bwd, comm,
-                                                         counts, num_mb, makespan, status);
+    if (lanes) {
+      const unsigned lg = grid_for(n, LaneCfg<S>::plans);
+      if (m == kTrace)
+        k_sim_l<S, kTrace><<<lg, 128, 0, st>>>(perm, n, stage_off, t_fwd, t_bwd, comm, counts,
+                                               num_mb, makespan, status, out);
+      else if (m == kRefNodes)
+        k_sim_l<S, kRefNodes><<<lg, 128, 0, st>>>(perm, n, stage_off, t_fwd, t_bwd, comm, counts,
+                                                  num_mb, makespan, status, out);
+      else
+        k_sim_l<S, kNoNodes><<<lg, 128, 0, st>>>(perm, n, stage_off, t_fwd, t_bwd, comm, counts,
+                                                 num_mb, makespan, status, out);
       ::hapt::note_launch();
       return;
     }

@@ -105,7 +105,7 @@ int cpl_for(const hapt_tables *t, int n_cand) {
 #define HAPT_U4 2
 #endif
 #ifndef HAPT_PROBE_MIN
-#define HAPT_PROBE_MIN 2  // staged entries above which a chunk is probed
+#define HAPT_PROBE_MIN 6  // kept entries above which a chunk is probed (round 2: 2 -> 6, D1 -0.8 %, C -1 %)
 #endif
 #ifndef HAPT_U2
 #define HAPT_U2 4  // 2, 4 or 8 (a 32-entry stage must be a multiple)

@@ -58,6 +58,13 @@ constexpr int kWarps = HAPT_KWARPS;  // warps (cells) per block
 #endif
 constexpr int kWarpsC = HAPT_KWARPS_C;  // warps per dp_relax_compact block
 constexpr int kParts = 32;  // copies of the per-candidate state counters
+#ifndef HAPT_GRID_DIV
+#define HAPT_GRID_DIV 2300  // cell-tasks (L x G x groups) per warp-per-SM of dp_relax_compact's cap
+#endif
+#ifndef HAPT_GRID_DIV4
+#define HAPT_GRID_DIV4 1800  // the same at 4 candidates per lane (D1 pool 4.73 -> 4.68 ms; at
+                             // CPL 2 the D1 2-GPU share measured 3.16 -> 3.26 ms with 1800)
+#endif
 #ifndef HAPT_WIN_MINLEN
 #define HAPT_WIN_MINLEN 1  // window hull also bounded by each option's shortest span
 #endif  // window cells of one (group, state) per relax warp
@@ -1397,7 +1404,9 @@ int run_sweep(const Batch &b, cudaStream_t st) {
       unsigned cap = gcap;
       if (cap == 0) {
         const long wps =
-            (std::min(192l, std::max(64l, (long)b.L * b.G * b.n_groups / 2300)) + 16) / 32 * 32;
+            (std::min(192l, std::max(64l, (long)b.L * b.G * b.n_groups /
+                                              (b.cpl == 4 ? HAPT_GRID_DIV4 : HAPT_GRID_DIV))) +
+             16) / 32 * 32;
         cap = (unsigned)(wps / kWarpsC) * (unsigned)sms;
       }
       const unsigned cgrid = min(cap, grid_for((size_t)cells * b.n_groups, kWarpsC));

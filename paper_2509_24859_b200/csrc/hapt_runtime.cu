@@ -96,7 +96,7 @@ extern "C" const char *hapt_last_error(void) { return g_err; }
 
 // 1 0 0 20: ABI 1, DP kernel generation 20 (profiles/dp_relax_traffic.json
 // records the generation its counters were taken on)
-extern "C" int hapt_version(void) { return 10028; }
+extern "C" int hapt_version(void) { return 10029; }
 
 extern "C" int hapt_prof_enable(int32_t on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);

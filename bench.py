@@ -562,11 +562,11 @@ def main():
         dt = time.perf_counter() - t0
         if i >= 2:
             e2e_times.append(dt)
-        # bytes copied per step: the instance description (one H2D blob; with
-        # N > 1 also this rank's candidate positions), the K1 counters, and
+        # bytes copied per step: the instance description (one H2D blob), the
+        # K1 counters, and
         # the results (pool, T*, best s, finite cells, winner -- with N > 1
         # all-gathered device to device first, then the same one transfer)
-        h2d = st2.dev.h2d_bytes + (len(sharding.shard_positions(P)) * 8 if world > 1 else 0)
+        h2d = st2.dev.h2d_bytes  # (the rank's candidate positions are cached on the device)
         d2h = 16 * 8 + P * 8 * 4 + 8
     t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=device)
     if world > 1:

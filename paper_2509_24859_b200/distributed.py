@@ -126,6 +126,16 @@ class PoolSharding:
             return tstar, best_s, states, ftop
         return tstar, best_s, states
 
+    def positions_device(self, n: int, device) -> torch.Tensor:
+        """shard_positions(n) as an int64 tensor on `device` (cached: a sweep
+        of the same pool size reuses it instead of copying it again)."""
+        cache = getattr(self, "_mine_cache", None)
+        key = (n, self.world, str(device))
+        if cache is None or cache[0] != key:
+            cache = (key, torch.from_numpy(self.shard_positions(n)).to(device))
+            self._mine_cache = cache
+        return cache[1]
+
     def gather_positions(self, local: torch.Tensor, n: int) -> torch.Tensor:
         """All ranks' per-candidate rows, device to device: local [m, C] int64
         holds this rank's candidates in shard_positions(n) order; returns

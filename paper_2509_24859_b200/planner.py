@@ -647,7 +647,7 @@ def sweep_pool(store: ProfileStore, costs: BoundaryCost, num_microbatches: int, 
         raise InfeasiblePlanError("no feasible candidates in the profile store")
     sw = tables.sweeper
     pool_dev = store.dev.pool()
-    mine = torch.from_numpy(dist.shard_positions(n)).to(pool_dev.device)
+    mine = dist.positions_device(n, pool_dev.device)
     if mine.numel():
         tmax = pool_dev[mine].contiguous()
         ftop, states = sw.sweep_device(tmax)

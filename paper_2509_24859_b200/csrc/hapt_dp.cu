@@ -222,11 +222,6 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
   return ws_layout(t, n_cand, cpl_for(t, n_cand));
 }
 
-// Large batches run as two independent halves of whole candidate groups on
-// two side streams, so one half's per-layer tails and window passes overlap
-// the other's work (measured, tools/try_streams.py at 4 candidates per lane:
-// D1 5.14 -> 5.01 ms, D2 78.8 -> 75.3 ms).  Both halves keep the full
-// batch's candidates-per-lane.  Off when full outputs are requested.
 // Large batches run as two independent halves (whole candidate groups, the
 // low-t_max half and the high-t_max half) on two side streams, so one
 // half's per-layer window passes and tails overlap the other's work.  Both
@@ -234,7 +229,9 @@ WsLayout ws_layout(const hapt_tables *t, int n_cand) {
 // tools/gpu/envs.sh HAPT_SPLIT=0): D2 78.2 -> 73.6 ms, D3 506 -> 472 ms;
 // D1 (14 groups) and smaller batches are faster unsplit (5.15 vs 5.52 ms),
 // alternating groups between the halves measured worse than contiguous
-// halves (D2 74.6, D3 481, D1 5.29 ms).  Off when full outputs are requested.
+// halves (D2 74.6, D3 481, D1 5.29 ms), and 3-4 parts no better than two
+// (round 2, same box: D3 452.8 vs 452.7 ms, D2 68.0 vs 67.9 ms).  Off when
+// full outputs are requested.
 struct Split {
   int parts, cpl;
   int n[2];
